@@ -1,0 +1,92 @@
+// hierarchy.cuh — the multilevel hierarchy (Hierarchy/Level of
+// hierarchy.hpp:46-64) owned by one C-ABI handle: device operators, host
+// mirrors of the topology, and the setup / vcycle / pcg drivers.
+#pragma once
+
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "setup_kernels.cuh"
+#include "solve.cuh"
+#include "sparse.cuh"
+
+namespace lsb {
+
+struct HostCsr {
+  int64_t nr = 0, nc = 0;
+  std::vector<int64_t> off, col;
+  std::vector<double> val;
+};
+
+struct Level {
+  DevCsr A, G, P;
+  Sell A_sell;
+  bool has_interp = false;
+  double thresh = 0.0;
+  // topology (host mirror + device copy)
+  std::vector<int32_t> h_omega_off, h_omega, h_gamma_off, h_gamma;
+  std::vector<int64_t> colors;
+  int64_t n_colors = 0, n_mult = 0;
+  DevTopo topo;
+  DevSmoother sm;
+  DevInterp ip;
+  DBuf<int32_t> col_agg;  // coarse column -> aggregate
+  DBuf<int32_t> mult;     // row multiplicities of G (export)
+  SchwarzView schwarz_view() const;
+  InterpView interp_view() const;
+};
+
+struct StageTime {
+  std::string name;
+  double ms;
+};
+
+struct Hierarchy {
+  std::vector<Level> levels;
+  DBuf<double> coarse_inv;
+  int64_t n_coarse = 0;
+  lsamgdd_params params{};
+  std::vector<uint64_t> ratios;
+  std::vector<lsamgdd_level_summary> summary;
+  DevCsr g0;           // the factor given to setup (pcg's default operator)
+  Sell g0_sell, g0t_sell;
+  std::vector<StageTime> timings;
+  int device = 0;
+  cudaStream_t stream = nullptr;  // setup stream
+  mutable std::mutex mu;          // guards lazily built export caches
+  ~Hierarchy();
+};
+
+// setup(g0, params) — hierarchy.hpp:106-200 plus the config hooks.
+Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* params);
+
+// Per-call solve workspace (concurrent calls on one handle each own one).
+struct SolveWs {
+  cudaStream_t s = nullptr;
+  std::vector<DBuf<double>> e, res, rhs;  // per level
+  Reducer red;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // level-0 RAS / RAS-T brackets
+  bool timing = false;
+  explicit SolveWs(const Hierarchy& h);
+  ~SolveWs();
+};
+
+// e = vcycle(h, level, r) on device pointers (hierarchy.hpp:205-227).
+void vcycle(const Hierarchy& h, SolveWs& ws, int64_t level, const double* r, double* e);
+
+struct PcgResult {
+  uint64_t iterations = 0;
+  bool converged = false;
+  std::vector<double> history;
+  double solve_seconds = 0.0;
+  int64_t launches = 0;
+};
+// pcg with apply_a = Gᵀ(G·), apply_b = vcycle (krylov.hpp:42-92). b, x device.
+PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, const double* b, double* x,
+              double tol, uint64_t maxit, lsamgdd_kernel_stats* stats);
+
+double operator_complexity(const Hierarchy& h);
+
+}  // namespace lsb

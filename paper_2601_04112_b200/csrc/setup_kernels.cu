@@ -1,0 +1,858 @@
+// setup_kernels.cu — batched per-aggregate setup stages (splitting.hpp,
+// smoother.hpp, hierarchy.hpp:72-95/193) on sm_100a.
+//
+// Each aggregate is one independent problem solved by a Team (a warp for
+// small problems, a CTA otherwise) over a private workspace in shared memory
+// when it fits, global memory otherwise. All FP64 arithmetic follows the
+// reference's operation order (see dense_dev.cuh), so panels, spectra and
+// factors are bit-identical to the reference's no-FMA build.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <numeric>
+
+#include "dense_dev.cuh"
+#include "setup_kernels.cuh"
+
+namespace lsb {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+int grid_for(int64_t n, int threads = kThreads) {
+  const int64_t cap = int64_t(sm_count()) * 16;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), cap)));
+}
+
+int bits_for(uint64_t v) {
+  int b = 1;
+  while (b < 64 && (uint64_t(1) << b) <= v) ++b;
+  return b;
+}
+
+__host__ __device__ inline int64_t r2(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+// position of node c in Ω_i = ω_i ‖ Γ_i (both ascending), or -1
+__device__ inline int lookup_sub(int c, const int32_t* om, int nw, const int32_t* ga, int ng) {
+  int lo = 0, hi = nw - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int v = om[mid];
+    if (v == c) return mid;
+    if (v < c)
+      lo = mid + 1;
+    else
+      hi = mid - 1;
+  }
+  lo = 0;
+  hi = ng - 1;
+  while (lo <= hi) {
+    const int mid = (lo + hi) >> 1;
+    const int v = ga[mid];
+    if (v == c) return nw + mid;
+    if (v < c)
+      lo = mid + 1;
+    else
+      hi = mid - 1;
+  }
+  return -1;
+}
+
+// ---- row sets ---------------------------------------------------------------
+
+__global__ void k_owner_keys(const int64_t* goff, const int32_t* gcol, int64_t m, const int32_t* node_agg,
+                             uint64_t* keys) {
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < m; r += int64_t(gridDim.x) * blockDim.x)
+    for (int64_t k = goff[r]; k < goff[r + 1]; ++k)
+      keys[k] = static_cast<uint64_t>(node_agg[gcol[k]]) * static_cast<uint64_t>(m) + static_cast<uint64_t>(r);
+}
+
+__global__ void k_rowset_fill(const uint64_t* keys, int64_t n, uint64_t m, int64_t* agg_cnt, int32_t* mult,
+                              int32_t* nz, int64_t* nz_pos_flag) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x)
+    nz_pos_flag[p] = (p == 0 || keys[p] != keys[p - 1]) ? 1 : 0;
+}
+
+__global__ void k_rowset_scatter(const uint64_t* keys, const int64_t* flag, const int64_t* pos, int64_t n, uint64_t m,
+                                 int64_t* agg_cnt, int32_t* mult, int32_t* nz) {
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < n; p += int64_t(gridDim.x) * blockDim.x) {
+    if (!flag[p]) continue;
+    const uint64_t key = keys[p];
+    const int64_t agg = static_cast<int64_t>(key / m);
+    const int64_t row = static_cast<int64_t>(key % m);
+    nz[pos[p]] = static_cast<int32_t>(row);
+    atomicAdd(reinterpret_cast<unsigned long long*>(&agg_cnt[agg + 1]), 1ull);
+    atomicAdd(&mult[row], 1);
+  }
+}
+
+__global__ void k_row_stats(const int64_t* goff, const int32_t* mult, int64_t m, unsigned long long* out3) {
+  // out3[0] = max mult, out3[1] = empty rows, out3[2] = max row nnz
+  unsigned long long mx = 0, empty = 0, mr = 0;
+  for (int64_t r = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; r < m; r += int64_t(gridDim.x) * blockDim.x) {
+    const unsigned long long mu = static_cast<unsigned long long>(mult[r]);
+    mx = mu > mx ? mu : mx;
+    empty += mu == 0 ? 1 : 0;
+    const unsigned long long len = static_cast<unsigned long long>(goff[r + 1] - goff[r]);
+    mr = len > mr ? len : mr;
+  }
+  atomicMax(&out3[0], mx);
+  atomicAdd(&out3[1], empty);
+  atomicMax(&out3[2], mr);
+}
+
+// ---- team problem dispatch ----------------------------------------------------
+
+struct TeamSlot {
+  int prob;
+  double* ws;
+};
+
+// ---- local GEVP (splitting.hpp:200-275) -----------------------------------------
+
+struct GevpArgs {
+  const int64_t* goff;
+  const int32_t* gcol;
+  const double* gval;
+  const int32_t* mult;
+  const int32_t* omega_off;
+  const int32_t* omega;
+  const int32_t* gamma_off;
+  const int32_t* gamma;
+  const int64_t* nz_off;
+  const int32_t* nz;
+  const int32_t* list;
+  int n_list;
+  int list_base;
+  int maxrow;
+  GevpParams p;
+  double* panel_tmp;
+  const int64_t* panel_off;  // per list entry (capacity nω²)
+  double* spec;
+  const int64_t* spec_off;   // per aggregate (capacity nω)
+  int32_t* kcols;            // per aggregate
+  int32_t* nspec;            // per aggregate
+  int32_t* status;           // per aggregate
+  double* gws;
+  int64_t ws_stride;
+};
+
+__host__ __device__ inline int64_t gevp_ws(int64_t nw, int64_t ng, int64_t maxrow) {
+  int64_t a = r2(nw * ng) + r2(ng * ng) + r2((maxrow + 1) / 2) + r2(maxrow);
+  if (ng > 0) a += r2(ng * ng) + r2(ng * nw) + r2(nw * nw) + r2(ng) + r2(ng * ng) + sym_eig_scratch(ng);
+  const int64_t b = r2(nw) + r2(nw * nw) + r2(nw * nw) + r2(nw) + spsd_gevp_scratch(nw);
+  return r2(8) + 2 * r2(nw * nw) + (a > b ? a : b);
+}
+
+template <class Team>
+__device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* ws) {
+  const int agg = g.list[idx];
+  const int32_t* om = g.omega + g.omega_off[agg];
+  const int nw = g.omega_off[agg + 1] - g.omega_off[agg];
+  const int32_t* ga = g.gamma + g.gamma_off[agg];
+  const int ng = g.gamma_off[agg + 1] - g.gamma_off[agg];
+  constexpr double tau_rel = 1e-10;
+  Arena ar{ws, 0};
+  double* slot = ar.take(8);
+  double* L = ar.take(int64_t(nw) * nw);
+  double* W = ar.take(int64_t(nw) * nw);
+  const Arena base = ar;
+
+  // ---- phase A: Grams straight from G's sparse rows (weighted_gram,
+  // splitting.hpp:102-115: rows ascending, zero w·x skipped).
+  Arena pa = base;
+  double* C = pa.take(int64_t(nw) * ng);
+  double* B = pa.take(int64_t(ng) * ng);
+  int* rpos = pa.take_int(g.maxrow);
+  double* rval = pa.take(g.maxrow);
+  t_fill(t, L, 0.0, 2 * r2(int64_t(nw) * nw));
+  t_fill(t, C, 0.0, r2(int64_t(nw) * ng) + r2(int64_t(ng) * ng));
+  const bool weighted_lhs = g.p.variant == 1;
+  for (int64_t ri = g.nz_off[agg]; ri < g.nz_off[agg + 1]; ++ri) {
+    const int r = g.nz[ri];
+    const double w = 1.0 / static_cast<double>(g.mult[r]);
+    const int64_t k0 = g.goff[r];
+    const int len = static_cast<int>(g.goff[r + 1] - k0);
+    for (int e = t.rank(); e < len; e += t.size()) {
+      rpos[e] = lookup_sub(g.gcol[k0 + e], om, nw, ga, ng);
+      rval[e] = g.gval[k0 + e];
+    }
+    t.sync();
+    const int pairs = len * len;
+    for (int pe = t.rank(); pe < pairs; pe += t.size()) {
+      const int e1 = pe / len, e2 = pe % len;
+      const int a = rpos[e1], b = rpos[e2];
+      if (a < 0 || b < 0) continue;
+      const double va = rval[e1], vb = rval[e2];
+      const double xw = w * va;
+      if (a < nw) {
+        if (b < nw) {
+          L[int64_t(a) * nw + b] += (weighted_lhs ? xw : va) * vb;
+          W[int64_t(a) * nw + b] += xw * vb;
+        } else {
+          C[int64_t(a) * ng + (b - nw)] += xw * vb;
+        }
+      } else if (b >= nw) {
+        B[int64_t(a - nw) * ng + (b - nw)] += xw * vb;
+      }
+    }
+    t.sync();
+  }
+  if (ng > 0) {
+    double* Pm = pa.take(int64_t(ng) * ng);
+    double* T = pa.take(int64_t(ng) * nw);
+    double* S = pa.take(int64_t(nw) * nw);
+    const int st = t_pseudo_inverse(t, ng, B, tau_rel, Pm, pa);
+    if (st) {
+      if (t.rank() == 0) g.status[agg] = st;
+      return;
+    }
+    // T = pinv·crossᵀ, S = cross·T (dense.hpp:47-59 with the transposed copy)
+    for (int64_t e = t.rank(); e < int64_t(ng) * nw; e += t.size()) {
+      const int i = static_cast<int>(e / nw), j = static_cast<int>(e % nw);
+      double s = 0.0;
+      for (int k = 0; k < ng; ++k) {
+        const double aik = Pm[int64_t(i) * ng + k];
+        if (aik == 0.0) continue;
+        s += aik * C[int64_t(j) * ng + k];
+      }
+      T[e] = s;
+    }
+    t.sync();
+    t_matmul(t, C, nw, ng, T, nw, S);
+    for (int64_t e = t.rank(); e < int64_t(nw) * nw; e += t.size()) W[e] -= S[e];
+    t.sync();
+  }
+  t_symmetrize(t, W, nw);
+
+  // ---- phase B: pencil, keep rule, MGS, sign rule
+  Arena pb = base;
+  double* values = pb.take(nw);
+  double* outv = pb.take(int64_t(nw) * nw);
+  double* panel = pb.take(int64_t(nw) * nw);  // column-major nw × keep
+  double* v = pb.take(nw);
+  int cnt = 0;
+  int st = t_spsd_gevp(t, nw, L, W, tau_rel, values, outv, &cnt, pb);
+  if (st) {
+    if (t.rank() == 0) g.status[agg] = st;
+    return;
+  }
+  for (int k = t.rank(); k < cnt; k += t.size()) g.spec[g.spec_off[agg] + k] = values[k];
+  if (t.rank() == 0) g.nspec[agg] = cnt;
+  for (int k = 0; k < cnt; ++k)
+    if (isnan(values[k])) {
+      if (t.rank() == 0) g.status[agg] = 3;
+      return;
+    }
+  int64_t max_modes = nw;
+  if (g.p.level > 0) {
+    max_modes = nw / g.p.ratio;
+    if (max_modes == 0) max_modes = 1;
+  } else if (g.p.level0_max_modes > 0) {
+    max_modes = g.p.level0_max_modes;
+  }
+  if (max_modes == 0) max_modes = 1;
+  int n_null = 0;
+  while (n_null < cnt && isinf(values[n_null])) ++n_null;
+  int above = n_null;
+  while (above < cnt && values[above] > g.p.thresh) ++above;
+  int severe = n_null;
+  while (severe < above && values[severe] >= g.p.must_keep) ++severe;
+  int64_t fin = min(int64_t(above - n_null), max_modes);
+  if (severe - n_null > fin) fin = severe - n_null;
+  int64_t keep = n_null + fin;
+  if (keep == 0) keep = 1;
+  if (keep > cnt) keep = cnt;
+  int cols = 0;
+  for (int k = 0; k < keep; ++k) {
+    for (int r = t.rank(); r < nw; r += t.size()) v[r] = outv[int64_t(k) * nw + r];
+    t.sync();
+    const double orig = sqrt(t_seq_dot(t, v, v, nw, slot));
+    for (int pass = 0; pass < 2; ++pass)
+      for (int c = 0; c < cols; ++c) {
+        const double* pc = panel + int64_t(c) * nw;
+        const double proj = t_seq_dot(t, pc, v, nw, slot);
+        for (int r = t.rank(); r < nw; r += t.size()) v[r] -= proj * pc[r];
+        t.sync();
+      }
+    const double nv = sqrt(t_seq_dot(t, v, v, nw, slot));
+    if (!(nv > 1e-12 * fmax(orig, 1e-300))) continue;
+    if (t.rank() == 0) {
+      int arg = 0;
+      for (int r = 1; r < nw; ++r)
+        if (fabs(v[r]) > fabs(v[arg])) arg = r;
+      slot[1] = v[arg] < 0.0 ? -1.0 : 1.0;
+    }
+    t.sync();
+    const double sign = slot[1];
+    for (int r = t.rank(); r < nw; r += t.size()) panel[int64_t(cols) * nw + r] = sign * v[r] / nv;
+    t.sync();
+    ++cols;
+  }
+  double* out = g.panel_tmp + g.panel_off[g.list_base + idx];
+  if (cols == 0) {
+    const double unit = 1.0 / sqrt(static_cast<double>(nw));
+    for (int r = t.rank(); r < nw; r += t.size()) out[r] = unit;
+    if (t.rank() == 0) g.kcols[agg] = 1;
+  } else {
+    for (int64_t e = t.rank(); e < int64_t(nw) * cols; e += t.size()) {
+      const int r = static_cast<int>(e / cols), c = static_cast<int>(e % cols);
+      out[e] = panel[int64_t(c) * nw + r];
+    }
+    if (t.rank() == 0) g.kcols[agg] = cols;
+  }
+  t.sync();
+}
+
+extern __shared__ double dyn_smem[];
+
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
+  WarpTeam t;
+  const int warp = threadIdx.x >> 5;
+  double* ws = dyn_smem + int64_t(warp) * g.ws_stride;
+  for (int idx = blockIdx.x * WPB + warp; idx < g.n_list; idx += gridDim.x * WPB) gevp_problem(t, g, idx, ws);
+}
+
+template <bool SMEM>
+__global__ void k_gevp_block(GevpArgs g) {
+  BlockTeam t;
+  double* ws = SMEM ? dyn_smem : g.gws + int64_t(blockIdx.x) * g.ws_stride;
+  for (int idx = blockIdx.x; idx < g.n_list; idx += gridDim.x) gevp_problem(t, g, idx, ws);
+}
+
+// ---- smoother blocks (smoother.hpp:38-58, dense.hpp:119-185) ---------------------
+
+struct SmArgs {
+  const int64_t* aoff;
+  const int32_t* acol;
+  const double* aval;
+  const int32_t* omega_off;
+  const int32_t* omega;
+  const int32_t* gamma_off;
+  const int32_t* gamma;
+  const int32_t* list;
+  int n_list;
+  int list_base;
+  const int64_t* sm_off;
+  double* sm_data;
+  int32_t* status;
+  double* gws;
+  int64_t ws_stride;
+};
+
+__host__ __device__ inline int64_t sm_ws(int64_t nw, int64_t ng) {
+  const int64_t m = nw + ng;
+  return r2(8) + 2 * r2(m * m) + r2(nw * m);
+}
+
+// Right-looking Cholesky of the full block (dense.hpp:135-153). Returns
+// false on a non-positive pivot.
+template <class Team>
+__device__ bool t_cholesky(const Team& t, double* l, int m, double* slot) {
+  for (int j = 0; j < m; ++j) {
+    if (t.rank() == 0) {
+      double d = l[int64_t(j) * m + j];
+      for (int k = 0; k < j; ++k) d -= l[int64_t(j) * m + k] * l[int64_t(j) * m + k];
+      slot[0] = d;
+    }
+    t.sync();
+    const double d = slot[0];
+    if (!(d > 0.0)) {
+      t.sync();
+      return false;
+    }
+    const double ljj = sqrt(d);
+    for (int i = j + 1 + t.rank(); i < m; i += t.size()) {
+      double s = l[int64_t(i) * m + j];
+      for (int k = 0; k < j; ++k) s -= l[int64_t(i) * m + k] * l[int64_t(j) * m + k];
+      l[int64_t(i) * m + j] = s / ljj;
+    }
+    if (t.rank() == 0) l[int64_t(j) * m + j] = ljj;
+    t.sync();
+  }
+  return true;
+}
+
+// factor_spd_block with its single jitter retry
+template <class Team>
+__device__ bool t_factor_spd(const Team& t, double* blk, const double* orig, int m, double* slot) {
+  if (t_cholesky(t, blk, m, slot)) return true;
+  if (t.rank() == 0) {
+    double maxd = 0.0;
+    for (int i = 0; i < m; ++i) maxd = fmax(maxd, fabs(orig[int64_t(i) * m + i]));
+    slot[1] = 1e-12 * maxd;
+  }
+  t.sync();
+  const double jitter = slot[1];
+  for (int64_t e = t.rank(); e < int64_t(m) * m; e += t.size())
+    blk[e] = orig[e] + ((e / m == e % m) ? jitter : 0.0);
+  t.sync();
+  return t_cholesky(t, blk, m, slot);
+}
+
+// column j of (L Lᵀ)⁻¹ by forward then backward substitution (dense.hpp:145-158)
+__device__ inline void chol_solve_unit(const double* l, int m, int j, double* x) {
+  for (int i = 0; i < m; ++i) x[i] = (i == j) ? 1.0 : 0.0;
+  for (int i = 0; i < m; ++i) {
+    double s = x[i];
+    for (int k = 0; k < i; ++k) s -= l[int64_t(i) * m + k] * x[k];
+    x[i] = s / l[int64_t(i) * m + i];
+  }
+  for (int ii = m; ii-- > 0;) {
+    double s = x[ii];
+    for (int k = ii + 1; k < m; ++k) s -= l[int64_t(k) * m + ii] * x[k];
+    x[ii] = s / l[int64_t(ii) * m + ii];
+  }
+}
+
+template <class Team>
+__device__ void smoother_problem(const Team& t, const SmArgs& g, int idx, double* ws) {
+  const int agg = g.list[idx];
+  const int32_t* om = g.omega + g.omega_off[agg];
+  const int nw = g.omega_off[agg + 1] - g.omega_off[agg];
+  const int32_t* ga = g.gamma + g.gamma_off[agg];
+  const int ng = g.gamma_off[agg + 1] - g.gamma_off[agg];
+  const int m = nw + ng;
+  Arena ar{ws, 0};
+  double* slot = ar.take(8);
+  double* blk = ar.take(int64_t(m) * m);
+  double* orig = ar.take(int64_t(m) * m);
+  double* X = ar.take(int64_t(nw) * m);
+  t_fill(t, orig, 0.0, int64_t(m) * m);
+  for (int i = t.rank(); i < m; i += t.size()) {  // submatrix(A, Ω, Ω)
+    const int node = i < nw ? om[i] : ga[i - nw];
+    for (int64_t k = g.aoff[node]; k < g.aoff[node + 1]; ++k) {
+      const int q = lookup_sub(g.acol[k], om, nw, ga, ng);
+      if (q >= 0) orig[int64_t(i) * m + q] = g.aval[k];
+    }
+  }
+  t.sync();
+  t_copy(t, blk, orig, int64_t(m) * m);
+  if (!t_factor_spd(t, blk, orig, m, slot)) {
+    if (t.rank() == 0) g.status[agg] = 1;
+    return;
+  }
+  for (int j = t.rank(); j < nw; j += t.size()) chol_solve_unit(blk, m, j, X + int64_t(j) * m);
+  t.sync();
+  double* out = g.sm_data + g.sm_off[agg];
+  const int64_t packed = int64_t(nw) * (nw + 1) / 2;
+  for (int64_t e = t.rank(); e < packed; e += t.size()) {
+    // e -> (i, j), i <= j, row-major packed upper
+    int i = 0;
+    int64_t rem = e;
+    while (rem >= nw - i) {
+      rem -= nw - i;
+      ++i;
+    }
+    const int j = i + static_cast<int>(rem);
+    out[e] = X[int64_t(j) * m + i];
+  }
+  for (int64_t e = t.rank(); e < int64_t(nw) * ng; e += t.size()) {
+    const int i = static_cast<int>(e / ng), gg = static_cast<int>(e % ng);
+    out[packed + e] = X[int64_t(i) * m + nw + gg];
+  }
+  t.sync();
+}
+
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_sm_warp(SmArgs g) {
+  WarpTeam t;
+  const int warp = threadIdx.x >> 5;
+  double* ws = dyn_smem + int64_t(warp) * g.ws_stride;
+  for (int idx = blockIdx.x * WPB + warp; idx < g.n_list; idx += gridDim.x * WPB) smoother_problem(t, g, idx, ws);
+}
+
+template <bool SMEM>
+__global__ void k_sm_block(SmArgs g) {
+  BlockTeam t;
+  double* ws = SMEM ? dyn_smem : g.gws + int64_t(blockIdx.x) * g.ws_stride;
+  for (int idx = blockIdx.x; idx < g.n_list; idx += gridDim.x) smoother_problem(t, g, idx, ws);
+}
+
+// ---- coarse factor -------------------------------------------------------------
+
+__global__ void k_coarse_dense(const int64_t* off, const int32_t* col, const double* val, int64_t n, double* d) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    for (int64_t k = off[i]; k < off[i + 1]; ++k) d[i * n + col[k]] = val[k];
+}
+
+__global__ void k_coarse_factor(double* blk, const double* orig, int m, double* X, double* inv, int32_t* status,
+                                double* slot) {
+  BlockTeam t;
+  if (!t_factor_spd(t, blk, orig, m, slot)) {
+    if (t.rank() == 0) *status = 1;
+    return;
+  }
+  for (int j = t.rank(); j < m; j += t.size()) chol_solve_unit(blk, m, j, X + int64_t(j) * m);
+  t.sync();
+  for (int64_t e = t.rank(); e < int64_t(m) * m; e += t.size()) {
+    const int i = static_cast<int>(e / m), j = static_cast<int>(e % m);
+    inv[e] = X[int64_t(j) * m + i];
+  }
+}
+
+// ---- P assembly ------------------------------------------------------------------
+
+__global__ void k_p_count(const int32_t* node_agg, const int32_t* node_pos, const int32_t* kc, const int64_t* poff,
+                          const double* panels, int64_t n, int64_t* cnt) {
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n; v += int64_t(gridDim.x) * blockDim.x) {
+    const int a = node_agg[v], r = node_pos[v], k = kc[a];
+    const double* row = panels + poff[a] + int64_t(r) * k;
+    int64_t c = 0;
+    for (int j = 0; j < k; ++j) c += row[j] != 0.0 ? 1 : 0;
+    cnt[v + 1] = c;
+  }
+}
+
+__global__ void k_p_fill(const int32_t* node_agg, const int32_t* node_pos, const int32_t* kc, const int64_t* poff,
+                         const double* panels, const int32_t* coff, const int64_t* off, int64_t n, int32_t* pcol,
+                         double* pval) {
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n; v += int64_t(gridDim.x) * blockDim.x) {
+    const int a = node_agg[v], r = node_pos[v], k = kc[a];
+    const double* row = panels + poff[a] + int64_t(r) * k;
+    int64_t o = off[v];
+    for (int j = 0; j < k; ++j)
+      if (row[j] != 0.0) {
+        pcol[o] = coff[a] + j;
+        pval[o] = row[j];
+        ++o;
+      }
+  }
+}
+
+__global__ void k_compact_panels(const int32_t* list, int n_list, const int32_t* omega_off, const int32_t* kc,
+                                 const int64_t* src_off, const double* src, const int64_t* dst_off, double* dst) {
+  for (int idx = blockIdx.x; idx < n_list; idx += gridDim.x) {
+    const int a = list[idx];
+    const int64_t cnt = int64_t(omega_off[a + 1] - omega_off[a]) * kc[a];
+    for (int64_t e = threadIdx.x; e < cnt; e += blockDim.x) dst[dst_off[a] + e] = src[src_off[idx] + e];
+  }
+}
+
+// workspace class of a problem: 0 warp+smem, 1 CTA+smem, 2 CTA+global
+inline int ws_class(int64_t w) { return w <= 3072 ? 0 : (w <= 26000 ? 1 : 2); }
+
+// Launch a batched per-aggregate stage in three workspace classes.
+template <class Args, class WarpK, class BlockSmemK, class BlockGlobK>
+void launch_classes(Args args, const std::vector<int32_t>& aggs, const std::vector<int64_t>& ws_need,
+                    WarpK warpk, BlockSmemK bsk, BlockGlobK bgk, std::vector<int32_t>& list_order, cudaStream_t s,
+                    std::vector<std::pair<int, int>>* ranges = nullptr) {
+  // classes: 0 warp+smem (ws <= 3072 doubles), 1 CTA+smem (<= 26000), 2 CTA+global
+  std::vector<int32_t> cls[3];
+  for (int32_t a : aggs) cls[ws_class(ws_need[a])].push_back(a);
+  list_order.clear();
+  for (int c = 0; c < 3; ++c) list_order.insert(list_order.end(), cls[c].begin(), cls[c].end());
+  DBuf<int32_t> dlist;
+  dlist.upload(list_order, s);
+  int64_t base = 0;
+  for (int c = 0; c < 3; ++c) {
+    const int cnt = static_cast<int>(cls[c].size());
+    if (cnt == 0) continue;
+    int64_t wmax = 0;
+    for (int32_t a : cls[c]) wmax = std::max(wmax, ws_need[a]);
+    wmax = r2(wmax);
+    Args g = args;
+    g.list = dlist.get() + base;
+    g.list_base = static_cast<int>(base);
+    g.n_list = cnt;
+    g.ws_stride = wmax;
+    if (c == 0) {
+      constexpr int WPB = 4;
+      const size_t smem = size_t(WPB) * wmax * 8;
+      LSB_CUDA(cudaFuncSetAttribute(warpk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      const int grid = static_cast<int>(std::min<int64_t>(ceil_div(cnt, WPB), int64_t(sm_count()) * 8));
+      warpk<<<grid, WPB * 32, smem, s>>>(g);
+      LSB_LAUNCH();
+    } else if (c == 1) {
+      const size_t smem = size_t(wmax) * 8;
+      LSB_CUDA(cudaFuncSetAttribute(bsk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      const int grid = static_cast<int>(std::min<int64_t>(cnt, int64_t(sm_count()) * 4));
+      bsk<<<grid, 128, smem, s>>>(g);
+      LSB_LAUNCH();
+    } else {
+      // global workspace slots; bound the footprint to ~2 GiB
+      const int64_t slots = std::max<int64_t>(1, std::min<int64_t>({int64_t(cnt), int64_t(sm_count()) * 2,
+                                                                    (int64_t(1) << 28) / std::max<int64_t>(wmax, 1)}));
+      DBuf<double> gws(slots * wmax, s);
+      g.gws = gws.get();
+      bgk<<<static_cast<int>(slots), 256, 0, s>>>(g);
+      LSB_LAUNCH();
+    }
+    if (ranges) ranges->push_back({static_cast<int>(base), cnt});
+    base += cnt;
+  }
+}
+
+}  // namespace
+
+void row_sets(const DevCsr& g, const DevTopo& topo, DevRowSets& rs, cudaStream_t s) {
+  const int64_t m = g.nr, nnz = g.nnz;
+  rs.mult.alloc(m, s);
+  rs.mult.zero(s);
+  rs.nz_off.alloc(topo.n_agg + 1, s);
+  DBuf<int64_t> cnt(topo.n_agg + 1, s);
+  cnt.zero(s);
+  int64_t uniq = 0;
+  if (nnz > 0) {
+    DBuf<uint64_t> k1(nnz, s), k2(nnz, s);
+    k_owner_keys<<<grid_for(m), kThreads, 0, s>>>(g.off.get(), g.col.get(), m, topo.node_agg.get(), k1.get());
+    LSB_LAUNCH();
+    size_t tmp = 0;
+    const int eb = bits_for(static_cast<uint64_t>(topo.n_agg) * static_cast<uint64_t>(m));
+    LSB_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp, k1.get(), k2.get(), nnz, 0, eb, s));
+    {
+      DBuf<unsigned char> tb(tmp, s);
+      LSB_CUDA(cub::DeviceRadixSort::SortKeys(tb.get(), tmp, k1.get(), k2.get(), nnz, 0, eb, s));
+    }
+    k1.release();
+    DBuf<int64_t> flag(nnz, s), pos(nnz, s);
+    k_rowset_fill<<<grid_for(nnz), kThreads, 0, s>>>(k2.get(), nnz, m, nullptr, nullptr, nullptr, flag.get());
+    LSB_LAUNCH();
+    tmp = 0;
+    LSB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, flag.get(), pos.get(), nnz, s));
+    {
+      DBuf<unsigned char> tb(tmp, s);
+      LSB_CUDA(cub::DeviceScan::ExclusiveSum(tb.get(), tmp, flag.get(), pos.get(), nnz, s));
+    }
+    uniq = read_scalar(pos.get() + nnz - 1, s) + read_scalar(flag.get() + nnz - 1, s);
+    rs.nz.alloc(uniq, s);
+    k_rowset_scatter<<<grid_for(nnz), kThreads, 0, s>>>(k2.get(), flag.get(), pos.get(), nnz, static_cast<uint64_t>(m),
+                                                         cnt.get(), rs.mult.get(), rs.nz.get());
+    LSB_LAUNCH();
+  }
+  size_t tmp = 0;
+  LSB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt.get(), rs.nz_off.get(), topo.n_agg + 1, s));
+  {
+    DBuf<unsigned char> tb(tmp, s);
+    LSB_CUDA(cub::DeviceScan::InclusiveSum(tb.get(), tmp, cnt.get(), rs.nz_off.get(), topo.n_agg + 1, s));
+  }
+  DBuf<unsigned long long> st(3, s);
+  st.zero(s);
+  if (m) k_row_stats<<<grid_for(m), kThreads, 0, s>>>(g.off.get(), rs.mult.get(), m, st.get());
+  LSB_LAUNCH();
+  const auto h = st.download(s);
+  rs.n_mult = static_cast<int64_t>(h[0]);
+  rs.empty_rows = static_cast<int64_t>(h[1]);
+  rs.max_row_nnz = static_cast<int64_t>(h[2]);
+}
+
+void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int32_t>& hoo,
+                    const std::vector<int32_t>& hgo, const std::vector<int64_t>& colors, int64_t n_colors,
+                    DevSmoother& sm, cudaStream_t s) {
+  const int64_t na = topo.n_agg;
+  sm.n_agg = na;
+  std::vector<int64_t> off(na + 1, 0), need(na);
+  std::vector<int32_t> aggs(na);
+  sm.max_omega = sm.max_sub = 0;
+  double b_ras = 0, b_rast = 0;
+  for (int64_t i = 0; i < na; ++i) {
+    const int64_t nw = hoo[i + 1] - hoo[i], ng = hgo[i + 1] - hgo[i];
+    off[i + 1] = off[i] + r2(nw * (nw + 1) / 2 + nw * ng);
+    need[i] = sm_ws(nw, ng);
+    aggs[i] = static_cast<int32_t>(i);
+    sm.max_omega = std::max(sm.max_omega, nw);
+    sm.max_sub = std::max(sm.max_sub, nw + ng);
+    const double blk = 8.0 * (nw * (nw + 1) / 2 + nw * ng);
+    b_ras += blk + 4.0 * (nw + ng) + 8.0 * (nw + ng) + 8.0 * nw;     // block + Ω ids + read r[Ω] + write e[ω]
+    b_rast += blk + 4.0 * (nw + ng) + 8.0 * nw + 16.0 * (nw + ng);   // block + Ω ids + read r[ω] + RMW e[Ω]
+  }
+  sm.bytes_ras = b_ras;
+  sm.bytes_rast = b_rast;
+  sm.off.upload(off, s);
+  sm.data.alloc(off[na], s);
+  DBuf<int32_t> status(na, s);
+  status.zero(s);
+  SmArgs g{};
+  g.aoff = a.off.get();
+  g.acol = a.col.get();
+  g.aval = a.val.get();
+  g.omega_off = topo.omega_off.get();
+  g.omega = topo.omega.get();
+  g.gamma_off = topo.gamma_off.get();
+  g.gamma = topo.gamma.get();
+  g.sm_off = sm.off.get();
+  g.sm_data = sm.data.get();
+  g.status = status.get();
+  std::vector<int32_t> order;
+  launch_classes(g, aggs, need, k_sm_warp<4>, k_sm_block<true>, k_sm_block<false>, order, s);
+  const auto hs = status.download(s);
+  for (int64_t i = 0; i < na; ++i)
+    if (hs[i]) raise(LSAMGDD_ERR_SETUP, "dense symmetric factorization failed for subdomain block of aggregate " +
+                                            std::to_string(i));
+  // colour-sorted aggregate order for the race-free RAS-T scatter
+  std::vector<int32_t> byc(na);
+  sm.color_off.assign(n_colors + 1, 0);
+  for (int64_t i = 0; i < na; ++i) ++sm.color_off[colors[i] + 1];
+  for (int64_t c = 0; c < n_colors; ++c) sm.color_off[c + 1] += sm.color_off[c];
+  std::vector<int64_t> cur(sm.color_off.begin(), sm.color_off.end() - 1);
+  for (int64_t i = 0; i < na; ++i) byc[cur[colors[i]]++] = static_cast<int32_t>(i);
+  sm.order.upload(byc, s);
+}
+
+void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int32_t>& hoo,
+                    const std::vector<int32_t>& hgo, const DevRowSets& rs, const std::vector<int64_t>& h_nz_off,
+                    const GevpParams& gp, DevInterp& ip, DevCsr& p, bool keep_spectra, cudaStream_t s) {
+  (void)h_nz_off;
+  const int64_t na = topo.n_agg;
+  const int64_t maxrow = std::max<int64_t>(rs.max_row_nnz, 1);
+  std::vector<int64_t> need(na), spec_off(na + 1, 0);
+  for (int64_t i = 0; i < na; ++i) {
+    const int64_t nw = hoo[i + 1] - hoo[i], ng = hgo[i + 1] - hgo[i];
+    need[i] = gevp_ws(nw, ng, maxrow);
+    spec_off[i + 1] = spec_off[i] + nw;
+  }
+  DBuf<int64_t> d_spec_off;
+  d_spec_off.upload(spec_off, s);
+  DBuf<double> spec(spec_off[na], s);
+  DBuf<int32_t> kcols(na, s), nspec(na, s), status(na, s);
+  status.zero(s);
+  nspec.zero(s);
+  // chunk aggregates (id order) so the nω² panel scratch stays bounded
+  const int64_t budget = int64_t(1) << 27;  // doubles (1 GiB)
+  std::vector<int32_t> h_k(na, 0);
+  ip.panel_off.alloc(na + 1, s);
+  std::vector<int64_t> final_off(na + 1, 0);
+  struct Chunk {
+    std::vector<int32_t> order;
+    std::vector<int64_t> tmp_off;
+  };
+  DBuf<double> final_panels;
+  std::vector<std::pair<int64_t, int64_t>> chunks;
+  {
+    int64_t a0 = 0;
+    while (a0 < na) {
+      int64_t tot = 0, a1 = a0;
+      while (a1 < na) {
+        const int64_t nw = hoo[a1 + 1] - hoo[a1];
+        if (a1 > a0 && tot + nw * nw > budget) break;
+        tot += nw * nw;
+        ++a1;
+      }
+      chunks.push_back({a0, a1});
+      a0 = a1;
+    }
+  }
+  // first pass: run all chunks, keep each chunk's panels on the device
+  std::vector<DBuf<double>> chunk_panels(chunks.size());
+  std::vector<DBuf<int64_t>> chunk_off(chunks.size());
+  std::vector<DBuf<int32_t>> chunk_list(chunks.size());
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    const int64_t a0 = chunks[ci].first, a1 = chunks[ci].second;
+    std::vector<int32_t> aggs;
+    for (int64_t a = a0; a < a1; ++a) aggs.push_back(static_cast<int32_t>(a));
+    // classes decide the list order; panel scratch offsets follow that order
+    std::vector<int32_t> order;
+    {
+      std::vector<int32_t> cls[3];
+      for (int32_t a : aggs) cls[ws_class(need[a])].push_back(a);
+      for (int c = 0; c < 3; ++c) order.insert(order.end(), cls[c].begin(), cls[c].end());
+    }
+    std::vector<int64_t> toff(order.size() + 1, 0);
+    for (size_t k = 0; k < order.size(); ++k) {
+      const int64_t nw = hoo[order[k] + 1] - hoo[order[k]];
+      toff[k + 1] = toff[k] + r2(nw * nw);
+    }
+    chunk_panels[ci].alloc(toff.back(), s);
+    chunk_off[ci].upload(toff, s);
+    GevpArgs g{};
+    g.goff = gm.off.get();
+    g.gcol = gm.col.get();
+    g.gval = gm.val.get();
+    g.mult = rs.mult.get();
+    g.omega_off = topo.omega_off.get();
+    g.omega = topo.omega.get();
+    g.gamma_off = topo.gamma_off.get();
+    g.gamma = topo.gamma.get();
+    g.nz_off = rs.nz_off.get();
+    g.nz = rs.nz.get();
+    g.maxrow = static_cast<int>(maxrow);
+    g.p = gp;
+    g.panel_tmp = chunk_panels[ci].get();
+    g.panel_off = chunk_off[ci].get();
+    g.spec = spec.get();
+    g.spec_off = d_spec_off.get();
+    g.kcols = kcols.get();
+    g.nspec = nspec.get();
+    g.status = status.get();
+    std::vector<int32_t> lo;
+    launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, s);
+    chunk_list[ci].upload(lo, s);
+  }
+  const auto hs = status.download(s);
+  for (int64_t i = 0; i < na; ++i) {
+    if (hs[i] == 1) raise(LSAMGDD_ERR_EIG, "sym_eig: Jacobi iteration did not converge");
+    if (hs[i] == 2) raise(LSAMGDD_ERR_EIG, "sym_eig: non-finite eigenvalue");
+    if (hs[i] == 3) raise(LSAMGDD_ERR_EIG, "local_gevp: aggregate " + std::to_string(i) + ": NaN eigenvalue");
+  }
+  h_k = kcols.download(s);
+  ip.h_k = h_k;
+  std::vector<int32_t> coff(na + 1, 0);
+  for (int64_t i = 0; i < na; ++i) {
+    const int64_t nw = hoo[i + 1] - hoo[i];
+    final_off[i + 1] = final_off[i] + nw * h_k[i];
+    coff[i + 1] = coff[i] + h_k[i];
+  }
+  ip.n_coarse = coff[na];
+  ip.coarse_off.upload(coff, s);
+  ip.panel_off.upload(final_off, s);
+  ip.panels.alloc(std::max<int64_t>(final_off[na], 1), s);
+  for (size_t ci = 0; ci < chunks.size(); ++ci) {
+    const int n_list = static_cast<int>(chunks[ci].second - chunks[ci].first);
+    k_compact_panels<<<std::min(n_list, sm_count() * 8), 128, 0, s>>>(
+        chunk_list[ci].get(), n_list, topo.omega_off.get(), kcols.get(), chunk_off[ci].get(), chunk_panels[ci].get(),
+        ip.panel_off.get(), ip.panels.get());
+    LSB_LAUNCH();
+  }
+  chunk_panels.clear();
+  // spectra to the host mirror when requested
+  ip.spectra.clear();
+  if (keep_spectra) {
+    const auto hsp = spec.download(s);
+    const auto hn = nspec.download(s);
+    ip.spectra.resize(na);
+    for (int64_t i = 0; i < na; ++i) ip.spectra[i].assign(hsp.begin() + spec_off[i], hsp.begin() + spec_off[i] + hn[i]);
+  }
+  // assemble_P: CSR with exact zeros dropped
+  const int64_t n = topo.n_nodes;
+  p.nr = n;
+  p.nc = ip.n_coarse;
+  DBuf<int64_t> cnt(n + 1, s);
+  cnt.zero(s);
+  k_p_count<<<grid_for(n), kThreads, 0, s>>>(topo.node_agg.get(), topo.node_pos.get(), kcols.get(), ip.panel_off.get(),
+                                             ip.panels.get(), n, cnt.get());
+  LSB_LAUNCH();
+  p.off.alloc(n + 1, s);
+  size_t tmp = 0;
+  LSB_CUDA(cub::DeviceScan::InclusiveSum(nullptr, tmp, cnt.get(), p.off.get(), n + 1, s));
+  {
+    DBuf<unsigned char> tb(tmp, s);
+    LSB_CUDA(cub::DeviceScan::InclusiveSum(tb.get(), tmp, cnt.get(), p.off.get(), n + 1, s));
+  }
+  p.nnz = read_scalar(p.off.get() + n, s);
+  p.col.alloc(p.nnz, s);
+  p.val.alloc(p.nnz, s);
+  k_p_fill<<<grid_for(n), kThreads, 0, s>>>(topo.node_agg.get(), topo.node_pos.get(), kcols.get(), ip.panel_off.get(),
+                                            ip.panels.get(), ip.coarse_off.get(), p.off.get(), n, p.col.get(),
+                                            p.val.get());
+  LSB_LAUNCH();
+}
+
+void coarse_factor(const DevCsr& a, DBuf<double>& inv, cudaStream_t s) {
+  const int64_t m = a.nr;
+  DBuf<double> orig(m * m, s), blk(m * m, s), X(m * m, s), slot(8, s);
+  DBuf<int32_t> status(1, s);
+  status.zero(s);
+  orig.zero(s);
+  k_coarse_dense<<<grid_for(m), kThreads, 0, s>>>(a.off.get(), a.col.get(), a.val.get(), m, orig.get());
+  LSB_LAUNCH();
+  LSB_CUDA(cudaMemcpyAsync(blk.get(), orig.get(), m * m * 8, cudaMemcpyDeviceToDevice, s));
+  inv.alloc(m * m, s);
+  k_coarse_factor<<<1, 1024, 0, s>>>(blk.get(), orig.get(), static_cast<int>(m), X.get(), inv.get(), status.get(),
+                                     slot.get());
+  LSB_LAUNCH();
+  if (read_scalar(status.get(), s)) raise(LSAMGDD_ERR_SETUP, "dense symmetric factorization failed for coarsest-level matrix");
+}
+
+}  // namespace lsb

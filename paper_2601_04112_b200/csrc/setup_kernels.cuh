@@ -1,0 +1,79 @@
+// setup_kernels.cuh — batched per-aggregate setup stages on the device.
+#pragma once
+
+#include "common.cuh"
+#include "sparse.cuh"
+
+namespace lsb {
+
+// Per-level aggregate topology on the device (AggregateTopology,
+// aggregation.hpp:33-54): ω and Γ lists, both ascending, as in the reference.
+struct DevTopo {
+  int64_t n_nodes = 0, n_agg = 0;
+  DBuf<int32_t> omega_off, omega, gamma_off, gamma;
+  DBuf<int32_t> node_agg, node_pos;  // owner aggregate and position in its ω
+};
+
+// RowSets (splitting.hpp:26-30) on the device.
+struct DevRowSets {
+  DBuf<int32_t> mult;   // per G row
+  DBuf<int64_t> nz_off; // n_agg + 1
+  DBuf<int32_t> nz;     // G rows, ascending within an aggregate
+  int64_t n_mult = 0;
+  int64_t empty_rows = 0;
+  int64_t max_row_nnz = 0;
+};
+
+// compute_row_sets (splitting.hpp:53-84)
+void row_sets(const DevCsr& g, const DevTopo& topo, DevRowSets& rs, cudaStream_t s);
+
+// Schwarz storage of one level: per aggregate, the ω columns of the explicit
+// inverse of A(Ω,Ω) (the only part RAS and RAS-T read): the ω×ω block as a
+// packed upper triangle, then the ω×Γ block row-major.
+struct DevSmoother {
+  int64_t n_agg = 0;
+  DBuf<int64_t> off;      // n_agg + 1 (doubles)
+  DBuf<double> data;
+  DBuf<int32_t> order;    // aggregates sorted by colour
+  std::vector<int64_t> color_off;  // host, n_colors + 1
+  int64_t max_omega = 0, max_sub = 0;
+  double bytes_ras = 0, bytes_rast = 0;  // algorithmic bytes per sweep
+};
+
+// build_smoother (smoother.hpp:38-58): extract A(Ω,Ω), Cholesky with the
+// jitter retry of factor_spd_block (dense.hpp:175-185), explicit ω columns of
+// the inverse. Throws SetupError for the first failing aggregate.
+void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int32_t>& h_omega_off,
+                    const std::vector<int32_t>& h_gamma_off, const std::vector<int64_t>& colors, int64_t n_colors,
+                    DevSmoother& sm, cudaStream_t s);
+
+struct GevpParams {
+  double thresh;
+  double must_keep;
+  int variant;
+  int level;
+  int64_t ratio;
+  int64_t level0_max_modes;
+};
+
+// Interpolation of one level: dense panels (nω_i × k_i, row-major) plus P
+// in CSR with exact zeros dropped (assemble_P, hierarchy.hpp:72-95).
+struct DevInterp {
+  int64_t n_coarse = 0;
+  std::vector<int32_t> h_k;  // k_i
+  DBuf<int32_t> coarse_off;  // n_agg + 1
+  DBuf<int64_t> panel_off;   // n_agg + 1
+  DBuf<double> panels;
+  std::vector<std::vector<double>> spectra;  // per aggregate (host)
+};
+
+// local_gevp for every aggregate (splitting.hpp:200-275) + assemble_P.
+void local_gevp_all(const DevCsr& g, const DevTopo& topo, const std::vector<int32_t>& h_omega_off,
+                    const std::vector<int32_t>& h_gamma_off, const DevRowSets& rs, const std::vector<int64_t>& h_nz_off,
+                    const GevpParams& gp, DevInterp& ip, DevCsr& p, bool keep_spectra, cudaStream_t s);
+
+// Dense Cholesky of the coarsest matrix with the jitter retry, returning the
+// full explicit inverse (row-major) for the coarse solve (hierarchy.hpp:193).
+void coarse_factor(const DevCsr& a, DBuf<double>& inv, cudaStream_t s);
+
+}  // namespace lsb

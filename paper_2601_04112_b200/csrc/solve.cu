@@ -1,0 +1,378 @@
+// solve.cu — the V-cycle and PCG hot loop on sm_100a.
+//
+// The level-0 Schwarz sweep is the dominant HBM stream of the solve
+// (75-80% of the reference's solve time). Each warp
+// stages one aggregate's inverse block (the ω columns only: packed ω×ω upper
+// triangle + ω×Γ, the part RAS/RAS-T read) and its residual patch in shared
+// memory with coalesced loads, then one lane per output row forms its dot
+// product. Grids are persistent, sized in multiples of the SM count.
+#include <algorithm>
+
+#include "solve.cuh"
+
+namespace lsb {
+
+namespace {
+
+extern __shared__ double smem_solve[];
+
+__device__ __forceinline__ int64_t pidx(int i, int j, int nw) {  // i <= j, row-major packed upper
+  return int64_t(i) * nw - (int64_t(i) * (i - 1)) / 2 + (j - i);
+}
+
+// MODE 0: RAS overwrite, 1: RAS accumulate, 2: RAS-T accumulate
+template <int MODE, class Team>
+__device__ __forceinline__ void schwarz_one(const Team& t, const SchwarzView& v, int a, const double* __restrict__ r,
+                                            double* __restrict__ e, double* sb, double* sr) {
+  const int32_t* om = v.omega + v.omega_off[a];
+  const int nw = v.omega_off[a + 1] - v.omega_off[a];
+  const int32_t* ga = v.gamma + v.gamma_off[a];
+  const int ng = v.gamma_off[a + 1] - v.gamma_off[a];
+  const int m = nw + ng;
+  const int64_t p0 = int64_t(nw) * (nw + 1) / 2;
+  const int64_t nblk = p0 + int64_t(nw) * ng;
+  const double* blk = v.sm_data + v.sm_off[a];
+  if (MODE < 2) {
+    for (int i = t.rank(); i < m; i += t.size()) sr[i] = __ldg(&r[i < nw ? om[i] : ga[i - nw]]);
+  } else {
+    for (int i = t.rank(); i < nw; i += t.size()) sr[i] = __ldg(&r[om[i]]);
+  }
+  const double* B = blk;
+  if (sb) {
+    for (int64_t q = t.rank(); q < nblk; q += t.size()) sb[q] = __ldcs(&blk[q]);
+    B = sb;
+  }
+  t.sync();
+  if (MODE < 2) {
+    for (int i = t.rank(); i < nw; i += t.size()) {
+      double s = 0.0;
+      for (int j = 0; j < nw; ++j) s += B[i <= j ? pidx(i, j, nw) : pidx(j, i, nw)] * sr[j];
+      const double* rowg = B + p0 + int64_t(i) * ng;
+      for (int g = 0; g < ng; ++g) s += rowg[g] * sr[nw + g];
+      if (MODE == 0)
+        e[om[i]] = s;
+      else
+        e[om[i]] += s;
+    }
+  } else {
+    for (int j = t.rank(); j < m; j += t.size()) {
+      double s = 0.0;
+      if (j < nw) {
+        for (int i = 0; i < nw; ++i) s += B[i <= j ? pidx(i, j, nw) : pidx(j, i, nw)] * sr[i];
+        e[om[j]] += s;
+      } else {
+        const int g = j - nw;
+        for (int i = 0; i < nw; ++i) s += B[p0 + int64_t(i) * ng + g] * sr[i];
+        e[ga[g]] += s;
+      }
+    }
+  }
+  t.sync();
+}
+
+template <int MODE, int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_schwarz_warp(SchwarzView v, const int32_t* list, int64_t count,
+                                                           const double* r, double* e, int stage, int rstage) {
+  WarpTeam t;
+  const int warp = threadIdx.x >> 5;
+  double* sb = smem_solve + int64_t(warp) * (stage + rstage);
+  double* sr = sb + stage;
+  for (int64_t idx = int64_t(blockIdx.x) * WPB + warp; idx < count; idx += int64_t(gridDim.x) * WPB) {
+    const int a = list ? list[idx] : static_cast<int>(idx);
+    schwarz_one<MODE>(t, v, a, r, e, sb, sr);
+  }
+}
+
+template <int MODE>
+__global__ void k_schwarz_block(SchwarzView v, const int32_t* list, int64_t count, const double* r, double* e,
+                                int stage, int rstage) {
+  BlockTeam t;
+  double* sb = stage > 0 ? smem_solve : nullptr;
+  double* sr = smem_solve + stage;
+  for (int64_t idx = blockIdx.x; idx < count; idx += gridDim.x) {
+    const int a = list ? list[idx] : static_cast<int>(idx);
+    schwarz_one<MODE>(t, v, a, r, e, sb, sr);
+  }
+}
+
+template <int MODE>
+void schwarz_launch(const SchwarzView& v, const int32_t* list, int64_t count, const double* r, double* e,
+                    cudaStream_t s) {
+  if (count == 0) return;
+  const int64_t max_blk = v.max_omega * (v.max_omega + 1) / 2 + v.max_omega * (v.max_sub - v.max_omega);
+  const int rstage = static_cast<int>((v.max_sub + 1) & ~int64_t(1));
+  if (max_blk <= 2048 && v.max_sub <= 512) {
+    constexpr int WPB = 8;
+    const int stage = static_cast<int>((max_blk + 1) & ~int64_t(1));
+    const size_t smem = size_t(WPB) * (stage + rstage) * 8;
+    static bool attr_set = false;
+    if (!attr_set) {
+      LSB_CUDA(cudaFuncSetAttribute(k_schwarz_warp<MODE, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      attr_set = true;
+    }
+    const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / std::max<size_t>(smem, 1)));
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(count, WPB), sm_count() * per_sm)));
+    k_schwarz_warp<MODE, WPB><<<grid, WPB * 32, smem, s>>>(v, list, count, r, e, stage, rstage);
+  } else {
+    const int stage = max_blk <= 24000 ? static_cast<int>((max_blk + 1) & ~int64_t(1)) : 0;
+    const size_t smem = size_t(stage + rstage) * 8;
+    static bool attr_set_b = false;
+    if (!attr_set_b) {
+      LSB_CUDA(cudaFuncSetAttribute(k_schwarz_block<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr_set_b = true;
+    }
+    const int grid = static_cast<int>(std::min<int64_t>(count, int64_t(sm_count()) * 4));
+    k_schwarz_block<MODE><<<grid, 256, smem, s>>>(v, list, count, r, e, stage, rstage);
+  }
+  LSB_LAUNCH();
+}
+
+__global__ void k_restrict(InterpView v, const double* __restrict__ res, double* __restrict__ rc) {
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < v.n_coarse; c += int64_t(gridDim.x) * blockDim.x) {
+    const int a = v.col_agg[c];
+    const int j = static_cast<int>(c - v.coarse_off[a]);
+    const int k = v.coarse_off[a + 1] - v.coarse_off[a];
+    const double* pan = v.panels + v.panel_off[a];
+    const int32_t* om = v.omega + v.omega_off[a];
+    const int nw = v.omega_off[a + 1] - v.omega_off[a];
+    double s = 0.0;
+    for (int rr = 0; rr < nw; ++rr) {
+      const double x = res[om[rr]];
+      if (x == 0.0) continue;
+      s += pan[int64_t(rr) * k + j] * x;
+    }
+    rc[c] = s;
+  }
+}
+
+__global__ void k_prolong(InterpView v, const double* __restrict__ ec, double* __restrict__ e) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < v.n_fine; i += int64_t(gridDim.x) * blockDim.x) {
+    const int a = v.node_agg[i];
+    const int rr = v.node_pos[i];
+    const int k = v.coarse_off[a + 1] - v.coarse_off[a];
+    const double* row = v.panels + v.panel_off[a] + int64_t(rr) * k;
+    const double* x = ec + v.coarse_off[a];
+    double s = 0.0;
+    for (int j = 0; j < k; ++j) s += row[j] * x[j];
+    e[i] += s;
+  }
+}
+
+__global__ void k_dense_mv(const double* __restrict__ m, int64_t n, const double* __restrict__ r, double* __restrict__ e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+    double s = 0.0;
+    for (int64_t j = lane; j < n; j += 32) s += m[i * n + j] * r[j];
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) e[i] = s;
+  }
+}
+
+int grid_for(int64_t n, int threads = 256) {
+  const int64_t cap = int64_t(sm_count()) * 16;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), cap)));
+}
+
+// ---- deterministic reductions ----------------------------------------------------
+
+constexpr int kRedThreads = 256;
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x < 32) {
+    s = lane < (blockDim.x >> 5) ? sh[lane] : 0.0;
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
+  return s;  // valid in thread 0
+}
+
+// Returns true in thread 0 of the last block to finish, with the total.
+__device__ bool finish_reduction(double block_total, double* partial, unsigned int* ticket, double* total) {
+  __shared__ bool last;
+  __shared__ double sh[32];
+  if (threadIdx.x == 0) {
+    partial[blockIdx.x] = block_total;
+    __threadfence();
+    const unsigned int t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  double v = 0.0;
+  for (int b = threadIdx.x; b < static_cast<int>(gridDim.x); b += blockDim.x) v += __ldcg(&partial[b]);
+  const double s = block_sum(v, sh);
+  if (threadIdx.x == 0) {
+    *total = s;
+    *ticket = 0;
+  }
+  return threadIdx.x == 0;
+}
+
+__device__ __forceinline__ void chunk_of(int64_t n, int64_t& lo, int64_t& hi) {
+  const int64_t chunk = ((n + gridDim.x - 1) / gridDim.x + 31) & ~int64_t(31);
+  lo = min(n, int64_t(blockIdx.x) * chunk);
+  hi = min(n, lo + chunk);
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_dot(const double* x, const double* y, int64_t n, double* partial,
+                                                     unsigned int* ticket, double* out) {
+  __shared__ double sh[32];
+  int64_t lo, hi;
+  chunk_of(n, lo, hi);
+  double v = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) v += x[i] * y[i];
+  const double bt = block_sum(v, sh);
+  double tot;
+  if (finish_reduction(bt, partial, ticket, &tot)) *out = tot;
+}
+
+// ap = Gᵀ gp (SELL, thread per row) fused with <p, ap>; alpha = rz / pap
+__global__ void __launch_bounds__(kRedThreads) k_ap_dot(const int64_t* __restrict__ soff, const int32_t* __restrict__ len,
+                                                        const int32_t* __restrict__ col, const double* __restrict__ val,
+                                                        int64_t nr, const double* __restrict__ gp,
+                                                        const double* __restrict__ p, double* __restrict__ ap,
+                                                        double* partial, unsigned int* ticket, PcgScalars* sc) {
+  __shared__ double sh[32];
+  int64_t lo, hi;
+  chunk_of(nr, lo, hi);
+  double v = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    const int64_t base = soff[i >> 5] + (i & 31);
+    const int n = len[i];
+    double s = 0.0;
+    for (int k = 0; k < n; ++k) {
+      const int64_t e = base + int64_t(k) * 32;
+      s += __ldcs(&val[e]) * __ldg(&gp[__ldcs(&col[e])]);
+    }
+    ap[i] = s;
+    v += p[i] * s;
+  }
+  const double bt = block_sum(v, sh);
+  double tot;
+  if (finish_reduction(bt, partial, ticket, &tot)) {
+    sc->pap = tot;
+    sc->alpha = sc->rz / tot;
+  }
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_update_xr(double* __restrict__ x, double* __restrict__ r,
+                                                           const double* __restrict__ p, const double* __restrict__ ap,
+                                                           int64_t n, double* partial, unsigned int* ticket,
+                                                           PcgScalars* sc) {
+  __shared__ double sh[32];
+  const double alpha = sc->alpha;
+  int64_t lo, hi;
+  chunk_of(n, lo, hi);
+  double v = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+    x[i] += alpha * p[i];
+    const double ri = r[i] + (-alpha) * ap[i];
+    r[i] = ri;
+    v += ri * ri;
+  }
+  const double bt = block_sum(v, sh);
+  double tot;
+  if (finish_reduction(bt, partial, ticket, &tot)) sc->rn2 = tot;
+}
+
+__global__ void __launch_bounds__(kRedThreads) k_rz(const double* r, const double* z, int64_t n, double* partial,
+                                                    unsigned int* ticket, PcgScalars* sc, int first) {
+  __shared__ double sh[32];
+  int64_t lo, hi;
+  chunk_of(n, lo, hi);
+  double v = 0.0;
+  for (int64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) v += r[i] * z[i];
+  const double bt = block_sum(v, sh);
+  double tot;
+  if (finish_reduction(bt, partial, ticket, &tot)) {
+    sc->rz_next = tot;
+    if (!first) sc->beta = tot / sc->rz;
+    sc->rz = tot;
+  }
+}
+
+__global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z, int64_t n, const PcgScalars* sc,
+                           int first) {
+  const double beta = sc->beta;
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    p[i] = first ? z[i] : z[i] + beta * p[i];
+}
+
+}  // namespace
+
+void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumulate, cudaStream_t s) {
+  if (accumulate)
+    schwarz_launch<1>(v, nullptr, v.n_agg, r, e, s);
+  else
+    schwarz_launch<0>(v, nullptr, v.n_agg, r, e, s);
+}
+
+void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, const double* r, double* e,
+                  cudaStream_t s) {
+  for (size_t c = 0; c + 1 < color_off.size(); ++c)
+    schwarz_launch<2>(v, v.order + color_off[c], color_off[c + 1] - color_off[c], r, e, s);
+}
+
+void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s) {
+  if (v.n_coarse == 0) return;
+  k_restrict<<<grid_for(v.n_coarse), 256, 0, s>>>(v, res, rc);
+  LSB_LAUNCH();
+}
+
+void prolong_add(const InterpView& v, const double* ec, double* e, cudaStream_t s) {
+  if (v.n_fine == 0) return;
+  k_prolong<<<grid_for(v.n_fine), 256, 0, s>>>(v, ec, e);
+  LSB_LAUNCH();
+}
+
+void dense_matvec(const double* m, int64_t n, const double* r, double* e, cudaStream_t s) {
+  if (n == 0) return;
+  const int grid = static_cast<int>(std::min<int64_t>(ceil_div(n, 8), int64_t(sm_count()) * 8));
+  k_dense_mv<<<grid, 256, 0, s>>>(m, n, r, e);
+  LSB_LAUNCH();
+}
+
+void Reducer::init(cudaStream_t s) {
+  nblocks = sm_count() * 2;
+  partial.alloc(nblocks, s);
+  ticket.alloc(1, s);
+  ticket.zero(s);
+}
+
+void dot(const Reducer& red, const double* x, const double* y, int64_t n, double* out, cudaStream_t s) {
+  k_dot<<<red.nblocks, kRedThreads, 0, s>>>(x, y, n, red.partial.get(), red.ticket.get(), out);
+  LSB_LAUNCH();
+}
+
+void pcg_ap_dot(const Sell& gt, const double* gp, const double* p, double* ap, const Reducer& red, PcgScalars* sc,
+                cudaStream_t s) {
+  k_ap_dot<<<red.nblocks, kRedThreads, 0, s>>>(gt.slice_off.get(), gt.row_len.get(), gt.col.get(), gt.val.get(), gt.nr,
+                                               gp, p, ap, red.partial.get(), red.ticket.get(), sc);
+  LSB_LAUNCH();
+}
+
+void pcg_update_xr(const Reducer& red, double* x, double* r, const double* p, const double* ap, int64_t n,
+                   PcgScalars* sc, cudaStream_t s) {
+  k_update_xr<<<red.nblocks, kRedThreads, 0, s>>>(x, r, p, ap, n, red.partial.get(), red.ticket.get(), sc);
+  LSB_LAUNCH();
+}
+
+void pcg_rz(const Reducer& red, const double* r, const double* z, int64_t n, PcgScalars* sc, bool first,
+            cudaStream_t s) {
+  k_rz<<<red.nblocks, kRedThreads, 0, s>>>(r, z, n, red.partial.get(), red.ticket.get(), sc, first ? 1 : 0);
+  LSB_LAUNCH();
+}
+
+void pcg_update_p(double* p, const double* z, int64_t n, const PcgScalars* sc, bool first, cudaStream_t s) {
+  k_update_p<<<grid_for(n), 256, 0, s>>>(p, z, n, sc, first ? 1 : 0);
+  LSB_LAUNCH();
+}
+
+}  // namespace lsb

@@ -1,0 +1,75 @@
+// solve.cuh — V-cycle and PCG kernels (hierarchy.hpp:205-229, krylov.hpp:42-92).
+#pragma once
+
+#include "common.cuh"
+#include "setup_kernels.cuh"
+#include "sparse.cuh"
+
+namespace lsb {
+
+struct SchwarzView {
+  int64_t n_agg;
+  const int32_t* omega_off;
+  const int32_t* omega;
+  const int32_t* gamma_off;
+  const int32_t* gamma;
+  const int64_t* sm_off;
+  const double* sm_data;
+  const int32_t* order;  // colour-sorted aggregate ids
+  int64_t max_omega, max_sub;
+};
+
+// RAS (smoother.hpp:65-83, mode RAS): e[ω_i] = (A_i⁻¹ r[Ω_i])|ω  (accumulate
+// adds into e instead of overwriting). ω sets are disjoint: no atomics.
+void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumulate, cudaStream_t s);
+// RAS-T: e[Ω_i] += A_i⁻¹ [r[ω_i]; 0], launched colour by colour (subdomains of
+// one colour are disjoint, aggregation.hpp:197-229), so plain read-modify-
+// writes are race-free and the sum order is deterministic.
+void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, const double* r, double* e,
+                  cudaStream_t s);
+
+struct InterpView {
+  int64_t n_fine, n_coarse, n_agg;
+  const int32_t* node_agg;
+  const int32_t* node_pos;
+  const int32_t* omega_off;
+  const int32_t* omega;
+  const int32_t* coarse_off;
+  const int64_t* panel_off;
+  const double* panels;
+  const int32_t* col_agg;  // aggregate of every coarse column
+};
+
+// rc = Pᵀ res (spmv_transpose, sparse.hpp:125-137): owner-computes per coarse
+// column, fine rows in ascending order — bit-identical to the scatter.
+void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s);
+// e += P ec (spmv + axpy, hierarchy.hpp:220): per fine row, panel order.
+void prolong_add(const InterpView& v, const double* ec, double* e, cudaStream_t s);
+// e = M r with the explicit coarsest inverse
+void dense_matvec(const double* m, int64_t n, const double* r, double* e, cudaStream_t s);
+
+// Deterministic dot product: fixed grid, fixed-order tree, last-block final
+// sum. Writes the result to *out (device).
+struct Reducer {
+  int nblocks = 0;
+  DBuf<double> partial;
+  DBuf<unsigned int> ticket;
+  void init(cudaStream_t s);
+};
+
+struct PcgScalars {
+  double rz, pap, alpha, beta, rn2, rz_next, r0_2, pad;
+};
+
+void dot(const Reducer& red, const double* x, const double* y, int64_t n, double* out, cudaStream_t s);
+
+// PCG building blocks (krylov.hpp:61-80), scalars kept on the device.
+void pcg_ap_dot(const Sell& gt, const double* gp, const double* p, double* ap, const Reducer& red, PcgScalars* sc,
+                cudaStream_t s);
+void pcg_update_xr(const Reducer& red, double* x, double* r, const double* p, const double* ap, int64_t n,
+                   PcgScalars* sc, cudaStream_t s);
+void pcg_rz(const Reducer& red, const double* r, const double* z, int64_t n, PcgScalars* sc, bool first,
+            cudaStream_t s);
+void pcg_update_p(double* p, const double* z, int64_t n, const PcgScalars* sc, bool first, cudaStream_t s);
+
+}  // namespace lsb
