@@ -188,6 +188,17 @@ int lsamgdd_profile_pcg(const void* handle, const double* b, double tol, uint64_
                         double* x, int32_t memory, lsamgdd_report* report,
                         lsamgdd_kernel_stats* stats, char* err, size_t errlen);
 
+/* sym_eig (eigen.hpp:35-118) of one dense n×n row-major matrix through a
+ * device path of the batched eigensolver: 0 warp team, 1 CTA team, 2 CTA
+ * pipelined (TMA-prefetched rows). Values ascending, vectors column k. Used by
+ * the parity tests to pin each path bit-for-bit against the reference. */
+int lsamgdd_dense_sym_eig(int64_t n, const double* a, double* values, double* vectors, int32_t path, char* err,
+                          size_t errlen);
+
+/* Kernels this library has launched from the calling thread so far (graph
+ * replays counted per captured kernel). The bench's gpu_launches claim. */
+int64_t lsamgdd_launch_count(void);
+
 /* ---- synthetic inputs (BASELINE.json configs) ---- */
 /* mt19937_64(seed) + uniform_real_distribution(lo,hi), the CLI recipe of
  * lsamgdd_cli.cpp:103-107; host only. */

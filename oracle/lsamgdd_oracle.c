@@ -1643,3 +1643,9 @@ void oracle_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out)
     out[k] = c * (hi - lo) + lo;
   }
 }
+
+int oracle_eigen_threshold(double kappa, int64_t kc, int64_t n_mult, double* out, char* err, size_t errlen) {
+  GUARD_BEGIN
+  *out = eigen_threshold(kappa, kc, n_mult);
+  GUARD_END
+}

@@ -525,6 +525,10 @@ int ref_standard_aggregation(const lsamgdd_csr* a, int64_t* assignment, int64_t*
   });
 }
 
+int ref_eigen_threshold(double kappa, int64_t kc, int64_t n_mult, double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] { *out = eigen_threshold(kappa, kc, n_mult); });
+}
+
 void ref_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out) {
   std::mt19937_64 gen(seed);
   std::uniform_real_distribution<double> dist(lo, hi);

@@ -87,6 +87,14 @@ class CpuChecker:
         abi.check(st, err)
         return out, nagg.value
 
+    def eigen_threshold(self, kappa: float, kc: int, n_mult: int) -> float:
+        out = C.c_double()
+        err = C.create_string_buffer(_ERRLEN)
+        st = self.fn("eigen_threshold")(C.c_double(kappa), C.c_int64(kc), C.c_int64(n_mult), C.byref(out), err,
+                                        C.c_size_t(_ERRLEN))
+        abi.check(st, err)
+        return out.value
+
     def uniform(self, seed: int, n: int, lo: float = -1.0, hi: float = 1.0):
         out = np.empty(n)
         self.fn("uniform")(C.c_uint64(seed), C.c_double(lo), C.c_double(hi), C.c_int64(n), abi.ptr(out))

@@ -160,12 +160,13 @@ int32_t lsamgdd_device_available(void) { return device_ok() ? 1 : 0; }
 int lsamgdd_setup(const lsamgdd_csr* g0, const lsamgdd_params* params, void** out, char* err, size_t errlen) {
   *out = nullptr;
   return guarded(err, errlen, [&] {
-    require_device();
     lsamgdd_params p;
     if (params)
       p = *params;
     else
       lsamgdd_params_default(&p);
+    lsb::validate_setup(g0, &p);  // host-side InputError contract first (hierarchy.hpp:107-117)
+    require_device();
     *out = lsb::setup(g0, &p);
   });
 }
@@ -374,6 +375,21 @@ int lsamgdd_setup_timings(const void* handle, const char** names, double* ms, in
     }
   });
 }
+
+int lsamgdd_dense_sym_eig(int64_t n, const double* a, double* values, double* vectors, int32_t path, char* err,
+                          size_t errlen) {
+  return guarded(err, errlen, [&] {
+    require_device();
+    cudaStream_t s;
+    LSB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    const int st = dense_sym_eig(n, a, values, vectors, path, s);
+    cudaStreamDestroy(s);
+    if (st == 1) raise(LSAMGDD_ERR_EIG, "sym_eig: Jacobi iteration did not converge");
+    if (st == 2) raise(LSAMGDD_ERR_EIG, "sym_eig: non-finite eigenvalue");
+  });
+}
+
+int64_t lsamgdd_launch_count(void) { return launch_counter(); }
 
 void lsamgdd_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out) {
   std::mt19937_64 gen(seed);

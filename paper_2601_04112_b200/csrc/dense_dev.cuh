@@ -12,6 +12,8 @@
 //     touches rows/columns p and q only), two team barriers per rotation.
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace lsb {
@@ -21,6 +23,8 @@ namespace lsb {
 struct Arena {
   double* base;
   int64_t used;
+  double* fast = nullptr;   // optional shared-memory scratch (CTA teams, global workspace)
+  int64_t fast_cap = 0;     // doubles
   __device__ double* take(int64_t n) {
     double* p = base + used;
     used += (n + 1) & ~int64_t(1);
@@ -29,9 +33,272 @@ struct Arena {
   __device__ int* take_int(int64_t n) { return reinterpret_cast<int*>(take((n + 1) / 2)); }
 };
 
-// workspace doubles needed by t_sym_eig (excluding its outputs)
+// workspace doubles needed by t_sym_eig (excluding its outputs); includes the
+// rotation log of the pipelined CTA path
 __host__ __device__ inline int64_t sym_eig_scratch(int64_t n) {
-  return 2 * ((n * n + 1) & ~int64_t(1)) + 3 * ((n + 1) & ~int64_t(1)) + 4;
+  const int64_t ld = (n + 1) & ~int64_t(1);
+  return 2 * (n * ld + 2) + 3 * ((n + 1) & ~int64_t(1)) + 4 + ((n * (n - 1) + 1) & ~int64_t(1)) + 2;
+}
+
+// ---- pipelined CTA Jacobi for large n (global workspace) -----------------------------
+//
+// Same rotation sequence and arithmetic as eigen.hpp:35-118. The matrix is
+// kept as a full symmetric array in global memory (both triangles updated).
+// While row p is swept, index p's vector a(p,·) lives in shared memory; the
+// partner rows q are prefetched with cp.async into a ring of R shared buffers
+// (prefetch depth R-2, so a slot is only refilled after every thread has
+// passed the barrier that retires it), patched with the entries rotated after
+// their prefetch, and written back (row and mirrored column) right after their
+// rotation. Every rotation pairs (a(p,j), a(q,j)) for j ∉ {p,q}, and thread
+// j mod T owns pair j for the whole sweep, so the single-writer updates of a
+// rotation (a(p,q) = 0, d[q] += h, z[q] += h) are deferred to the next step
+// and each rotation costs one CTA barrier with a shared-memory critical path.
+// Eigenvector rotations are logged (s, tau) and applied per sweep, one row of
+// V per thread, off the critical path.
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+constexpr int kPipeThreads = 512;   // the pipelined path runs on exactly this CTA size
+
+// shared doubles of the pipelined path with R ring slots
+__host__ __device__ inline int64_t pipelined_smem_doubles(int64_t n, int R) {
+  const int64_t ld = (n + 1) & ~int64_t(1);
+  return (2 + 2 * R) * ld + 3 * ld + 16 + 3 * 2 * R * R;
+}
+
+__device__ long long* g_eig_prof = nullptr;  // optional per-phase cycle counters (test hook)
+
+// Returns 0/1/2 like t_sym_eig. A: global scratch n×ld (ld = n rounded to
+// even, 16-byte rows), Vt: global n×ld (Vᵀ, row k = eigenvector column k),
+// sm: shared scratch of pipelined_smem_doubles(n, R). Requires blockDim.x == 512.
+//
+// Ring protocol (R slots, depth D = R-2): at step q every thread issues its
+// cp.async pieces of rows q+D of A and Vᵀ into slot (q+D) mod R (whose
+// previous rows, q-2, were consumed before the barrier of step q-1), commits,
+// waits for row q (wait_group D) and meets the barrier. A row r of A in flight
+// can miss entries (r, q') rotated at steps q' in [r-D-1, r-1] (step r-D-1 may
+// still be writing while r's copy is issued); each such entry is recorded in
+// row r's patch list (indexed r mod 2R, reset at step r-R) and applied by the
+// entry's owner when row r is rotated. Rows of Vᵀ need no patches: within row
+// p's sweep, Vᵀ row q changes only at step q.
+template <int R>
+__device__ int cta_sym_eig_pipelined(int n, const double* m, double* vals, double* vecs, double* A, double* Vt,
+                                     double* sm) {
+  constexpr int D = R - 2, NL = 2 * R, T = kPipeThreads;
+  const int tid = threadIdx.x;
+  const int64_t ld = (n + 1) & ~int64_t(1);
+  double* pv = sm;                       // a(p,·)
+  double* vp = pv + ld;                  // Vᵀ row p
+  double* ring = vp + ld;                // R slots × (A row, Vᵀ row)
+  double* d = ring + int64_t(2 * R) * ld;
+  double* bb = d + ld;
+  double* z = bb + ld;
+  double* slot = z + ld;
+  double* pend_val = slot + 16;                                 // [NL][R]
+  int* pend_pos = reinterpret_cast<int*>(pend_val + NL * R);  // [NL][R]
+  __shared__ int pend_n[NL];
+  long long t_sm = 0, t_wait = 0, t_par = 0, t_rot = 0, tc = 0;
+  auto tick = [&](long long& acc) {
+    const long long now = clock64();
+    acc += now - tc;
+    tc = now;
+  };
+  for (int64_t e = tid; e < int64_t(n) * n; e += T) {  // full symmetric copy (eigen.hpp:44)
+    const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+    double val = m[e];
+    if (i != j) {
+      const int lo = i < j ? i : j, hi = i < j ? j : i;
+      val = 0.5 * (m[int64_t(lo) * n + hi] + m[int64_t(hi) * n + lo]);
+    }
+    A[int64_t(i) * ld + j] = val;
+    Vt[int64_t(i) * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  for (int i = tid; i < n; i += T) {
+    d[i] = bb[i] = m[int64_t(i) * n + i];
+    z[i] = 0.0;
+  }
+  __syncthreads();
+  const int chunks = static_cast<int>(ld / 2);  // 16-byte pieces per row
+  auto prefetch = [&](int row) {
+    if (row < n) {
+      double* dst = ring + int64_t(2 * (row % R)) * ld;
+      const double* srca = A + int64_t(row) * ld;
+      const double* srcv = Vt + int64_t(row) * ld;
+      for (int c = tid; c < chunks; c += T) {
+        cp_async16(dst + 2 * c, srca + 2 * c);
+        cp_async16(dst + ld + 2 * c, srcv + 2 * c);
+      }
+    }
+    cp_async_commit();
+  };
+  bool converged = false;
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    // Σ_{p<q} |a(p,q)| in the reference's order: rows staged in shared memory,
+    // summed sequentially by thread 0
+    double smv = 0.0;
+    tc = clock64();
+    for (int p = 0; p + 1 < n; ++p) {
+      for (int q = p + 1 + tid; q < n; q += T) ring[q] = A[int64_t(p) * ld + q];
+      __syncthreads();
+      if (tid == 0)
+        for (int q = p + 1; q < n; ++q) smv += fabs(ring[q]);
+      __syncthreads();
+    }
+    if (tid == 0) slot[0] = smv;
+    __syncthreads();
+    tick(t_sm);
+    smv = slot[0];
+    if (smv == 0.0) {
+      converged = true;
+      break;
+    }
+    const double tresh = sweep < 3 ? 0.2 * smv / static_cast<double>(static_cast<uint64_t>(n) * n) : 0.0;
+    for (int p = 0; p + 1 < n; ++p) {
+      for (int j = tid; j < n; j += T) {
+        pv[j] = A[int64_t(p) * ld + j];
+        vp[j] = Vt[int64_t(p) * ld + j];
+      }
+      if (tid < NL) pend_n[tid] = 0;
+      __syncthreads();
+      for (int k = 1; k <= D; ++k) prefetch(p + k);
+      double dp = d[p];
+      double zp = z[p];
+      int prev_q = -1, prev_zero = 0;
+      double prev_h = 0.0;
+      for (int q = p + 1; q < n; ++q) {
+        tick(t_rot);
+        prefetch(q + D);
+        cp_async_wait<D>();
+        __syncthreads();
+        tick(t_wait);
+        // single-owner writes deferred from step q-1 (their readers passed the barrier)
+        if (prev_q >= 0) {
+          if (prev_zero && (prev_q & (T - 1)) == tid) pv[prev_q] = 0.0;
+          if (tid == 0 && prev_h != 0.0) {
+            z[prev_q] += prev_h;
+            d[prev_q] += prev_h;
+          }
+        }
+        if (tid == 0) pend_n[(q + R) % NL] = 0;
+        const double* qv = ring + int64_t(2 * (q % R)) * ld;
+        const double* qvv = qv + ld;
+        const double apq = pv[q];
+        const double dq = d[q];
+        const double g = 100.0 * fabs(apq);
+        double h = 0.0;
+        int zero = 0;
+        if (sweep > 3 && fabs(dp) + g == fabs(dp) && fabs(dq) + g == fabs(dq)) {
+          zero = 1;
+        } else if (fabs(apq) > tresh) {
+          double hh = dq - dp;
+          double tt;
+          if (fabs(hh) + g == fabs(hh)) {
+            tt = apq / hh;
+          } else {
+            const double theta = 0.5 * hh / apq;
+            tt = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
+            if (theta < 0.0) tt = -tt;
+          }
+          const double c = 1.0 / sqrt(1.0 + tt * tt);
+          const double s = tt * c;
+          const double tau = s / (1.0 + c);
+          h = tt * apq;
+          zp -= h;
+          dp -= h;
+          zero = 1;
+          tick(t_par);
+          const int li = q % NL;
+          const int np = pend_n[li];
+          for (int j = tid; j < n; j += T) {
+            // eigenvectors: rotate(v(j,p), v(j,q)) (eigen.hpp:93)
+            const double vx = vp[j], vy = qvv[j];
+            vp[j] = vx - s * (vy + vx * tau);
+            Vt[int64_t(q) * ld + j] = vy + s * (vx - vy * tau);
+            if (j == p || j == q) continue;
+            double hy = qv[j];
+            for (int e = 0; e < np; ++e)
+              if (pend_pos[li * R + e] == j) hy = pend_val[li * R + e];
+            const double gx = pv[j];
+            const double nx = gx - s * (hy + gx * tau);
+            const double ny = hy + s * (gx - hy * tau);
+            pv[j] = nx;
+            A[int64_t(q) * ld + j] = ny;  // row q and its mirrored column
+            A[int64_t(j) * ld + q] = ny;
+            if (j > q && j < q + R) {  // row j may hold a stale (j, q) entry
+              const int lj = j % NL;
+              const int e = pend_n[lj]++;
+              pend_pos[lj * R + e] = q;
+              pend_val[lj * R + e] = ny;
+            }
+          }
+        }
+        prev_q = q;
+        prev_h = h;
+        prev_zero = zero;
+      }
+      tick(t_rot);
+      cp_async_wait<0>();
+      __syncthreads();
+      if (prev_zero && (prev_q & (T - 1)) == tid) pv[prev_q] = 0.0;
+      if (tid == 0) {
+        if (prev_h != 0.0) {
+          z[prev_q] += prev_h;
+          d[prev_q] += prev_h;
+        }
+        d[p] = dp;
+        z[p] = zp;
+      }
+      __syncthreads();
+      for (int j = tid; j < n; j += T) {  // index p's final vectors back to A (row and column) and Vᵀ
+        Vt[int64_t(p) * ld + j] = vp[j];
+        if (j == p) continue;
+        A[int64_t(p) * ld + j] = pv[j];
+        A[int64_t(j) * ld + p] = pv[j];
+      }
+      __syncthreads();
+    }
+    for (int i = tid; i < n; i += T) {
+      bb[i] += z[i];
+      d[i] = bb[i];
+      z[i] = 0.0;
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && g_eig_prof) {
+    g_eig_prof[0] += t_sm;
+    g_eig_prof[1] += t_wait;
+    g_eig_prof[2] += t_par;
+    g_eig_prof[3] += t_rot;
+  }
+  if (!converged) return 1;
+  for (int i = 0; i < n; ++i)
+    if (!isfinite(d[i])) return 2;
+  for (int k = tid; k < n; k += T) {
+    const double dk = d[k];
+    int pos = 0;
+    for (int i = 0; i < n; ++i)
+      if (d[i] < dk || (d[i] == dk && i < k)) ++pos;
+    vals[pos] = dk;
+    for (int i = 0; i < n; ++i) vecs[int64_t(i) * n + pos] = Vt[int64_t(k) * ld + i];
+  }
+  __syncthreads();
+  return 0;
+}
+
+__device__ inline int cta_sym_eig_pipelined_any(int n, const double* m, double* vals, double* vecs, double* A,
+                                                double* Vt, double* sm, int R) {
+  if (R >= 8) return cta_sym_eig_pipelined<8>(n, m, vals, vecs, A, Vt, sm);
+  if (R >= 6) return cta_sym_eig_pipelined<6>(n, m, vals, vecs, A, Vt, sm);
+  return cta_sym_eig_pipelined<4>(n, m, vals, vecs, A, Vt, sm);
 }
 
 template <class Team>
@@ -118,6 +385,18 @@ __device__ int t_sym_eig(const Team& t, int n, const double* m, double* vals, do
   if (n == 0) {
     t.sync();
     return 0;
+  }
+  if constexpr (!std::is_same<Team, WarpTeam>::value) {
+    if (ar.fast && n >= 48 && blockDim.x == kPipeThreads) {
+      int R = 8;
+      while (R > 4 && pipelined_smem_doubles(n, R) > ar.fast_cap) R -= 2;
+      if (pipelined_smem_doubles(n, R) <= ar.fast_cap) {
+        const int64_t ld = (n + 1) & ~int64_t(1);
+        double* A = ar.take(int64_t(n) * ld);
+        double* Vt = ar.take(int64_t(n) * ld);
+        return cta_sym_eig_pipelined_any(n, m, vals, vecs, A, Vt, ar.fast, R);
+      }
+    }
   }
   double* a = ar.take(nn);
   double* v = ar.take(nn);

@@ -14,6 +14,7 @@
 #include <memory>
 #include <numeric>
 
+#include "galerkin.cuh"
 #include "hierarchy.cuh"
 
 namespace lsb {
@@ -257,7 +258,9 @@ double eigen_threshold(double kappa, int64_t kc, int64_t n_mult) {  // splitting
   return std::max(0.1, t);
 }
 
-void validate(const lsamgdd_params* p, const lsamgdd_csr* g0) {  // hierarchy.hpp:107-117
+}  // namespace
+
+void validate_setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {  // hierarchy.hpp:107-117
   if (p->max_levels < 2) raise(LSAMGDD_ERR_INPUT, "setup: max_levels must be at least 2");
   if (p->coarse_size < 1) raise(LSAMGDD_ERR_INPUT, "setup: coarse_size must be positive");
   if (p->aggregation_passes < 1) raise(LSAMGDD_ERR_INPUT, "setup: aggregation_passes must be positive");
@@ -270,7 +273,11 @@ void validate(const lsamgdd_params* p, const lsamgdd_csr* g0) {  // hierarchy.hp
   if (g0->n_rows == 0 || g0->n_cols == 0) raise(LSAMGDD_ERR_INPUT, "setup: factor is empty");
   if (g0->n_rows >= (int64_t(1) << 31) || g0->n_cols >= (int64_t(1) << 31))
     raise(LSAMGDD_ERR_SIZE, "setup: dimensions must stay below 2^31");
+  if (p->level0_partition && p->level0_n_aggregates <= 0)
+    raise(LSAMGDD_ERR_INPUT, "build_topology: partition has no aggregates");
 }
+
+namespace {
 
 __global__ void k_col_agg(const int32_t* coff, int64_t n_agg, int32_t* col_agg) {
   for (int64_t a = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; a < n_agg; a += int64_t(gridDim.x) * blockDim.x)
@@ -323,7 +330,7 @@ Hierarchy::~Hierarchy() {
 }
 
 Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
-  validate(p, g0);
+  validate_setup(g0, p);
   auto h = std::make_unique<Hierarchy>();
   h->params = *p;
   h->params.level0_partition = nullptr;
@@ -384,7 +391,8 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
     gp.level0_max_modes = static_cast<int64_t>(p->level0_max_modes);
     local_gevp_all(cur.G, cur.topo, cur.h_omega_off, cur.h_gamma_off, rs, {}, gp, cur.ip, cur.P, p->keep_spectra != 0,
                    s);
-    cur.mult = std::move(rs.mult);
+    cur.mult.alloc(rs.mult.size(), s);
+    LSB_CUDA(cudaMemcpyAsync(cur.mult.get(), rs.mult.get(), rs.mult.bytes(), cudaMemcpyDeviceToDevice, s));
     cur.has_interp = true;
     cur.col_agg.alloc(std::max<int64_t>(cur.ip.n_coarse, 1), s);
     k_col_agg<<<std::max(1, static_cast<int>(std::min<int64_t>(ceil_div(n_agg, 256), 1024))), 256, 0, s>>>(
@@ -393,12 +401,8 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
     stage("local_gevp", t0);
     t0 = Clock::now();
     Level next;
-    csr_spgemm_symbolic(cur.G, cur.P, next.G, s);
-    {
-      DevCsr gt;
-      csr_transpose(next.G, gt, s);
-      csr_spgemm_symbolic(gt, next.G, next.A, s);
-    }
+    galerkin_gp(cur.G, cur.topo, cur.ip, next.G, s);
+    galerkin_gtg(next.G, rs, n_agg, cur.ip, cur.col_agg.get(), next.A, s);
     stage("galerkin", t0);
     if (next.A.nr >= cur.A.nr)
       raise(LSAMGDD_ERR_SETUP, "setup: stagnant coarsening at level " + std::to_string(ell) + " (" +
@@ -599,6 +603,7 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
   out.iterations = k;
   out.solve_seconds = ms_since(t0) / 1e3;
   out.launches = (launch_counter() - launches0) + graph_launches * per_iter - per_iter;
+  launch_counter() += graph_launches * per_iter - per_iter;  // graph replays launch the captured kernels
   if (stats) {
     *stats = lsamgdd_kernel_stats{};
     stats->schwarz_ms = sw_ms;

@@ -59,6 +59,9 @@ struct Hierarchy {
   ~Hierarchy();
 };
 
+// parameter / input checks of setup (hierarchy.hpp:107-117), host only
+void validate_setup(const lsamgdd_csr* g0, const lsamgdd_params* p);
+
 // setup(g0, params) — hierarchy.hpp:106-200 plus the config hooks.
 Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* params);
 

@@ -10,6 +10,8 @@
 
 #include <algorithm>
 #include <numeric>
+#include <cstdio>
+#include <cstdlib>
 
 #include "dense_dev.cuh"
 #include "setup_kernels.cuh"
@@ -146,14 +148,15 @@ __host__ __device__ inline int64_t gevp_ws(int64_t nw, int64_t ng, int64_t maxro
 }
 
 template <class Team>
-__device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* ws) {
+__device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* ws, double* fast = nullptr,
+                             int64_t fast_cap = 0) {
   const int agg = g.list[idx];
   const int32_t* om = g.omega + g.omega_off[agg];
   const int nw = g.omega_off[agg + 1] - g.omega_off[agg];
   const int32_t* ga = g.gamma + g.gamma_off[agg];
   const int ng = g.gamma_off[agg + 1] - g.gamma_off[agg];
   constexpr double tau_rel = 1e-10;
-  Arena ar{ws, 0};
+  Arena ar{ws, 0, fast, fast_cap};
   double* slot = ar.take(8);
   double* L = ar.take(int64_t(nw) * nw);
   double* W = ar.take(int64_t(nw) * nw);
@@ -315,11 +318,18 @@ __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
   for (int idx = blockIdx.x * WPB + warp; idx < g.n_list; idx += gridDim.x * WPB) gevp_problem(t, g, idx, ws);
 }
 
+constexpr int64_t kFastCap = 24 * 1024;  // shared doubles for the pipelined Jacobi (192 KiB)
+
 template <bool SMEM>
 __global__ void k_gevp_block(GevpArgs g) {
   BlockTeam t;
   double* ws = SMEM ? dyn_smem : g.gws + int64_t(blockIdx.x) * g.ws_stride;
-  for (int idx = blockIdx.x; idx < g.n_list; idx += gridDim.x) gevp_problem(t, g, idx, ws);
+  for (int idx = blockIdx.x; idx < g.n_list; idx += gridDim.x) {
+    if (SMEM)
+      gevp_problem(t, g, idx, ws);
+    else
+      gevp_problem(t, g, idx, ws, dyn_smem, kFastCap);
+  }
 }
 
 // ---- smoother blocks (smoother.hpp:38-58, dense.hpp:119-185) ---------------------
@@ -577,7 +587,9 @@ void launch_classes(Args args, const std::vector<int32_t>& aggs, const std::vect
                                                                     (int64_t(1) << 28) / std::max<int64_t>(wmax, 1)}));
       DBuf<double> gws(slots * wmax, s);
       g.gws = gws.get();
-      bgk<<<static_cast<int>(slots), 256, 0, s>>>(g);
+      const size_t fsm = size_t(kFastCap) * 8;
+      LSB_CUDA(cudaFuncSetAttribute(bgk, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(fsm)));
+      bgk<<<static_cast<int>(slots), 512, fsm, s>>>(g);
       LSB_LAUNCH();
     }
     if (ranges) ranges->push_back({static_cast<int>(base), cnt});
@@ -585,7 +597,62 @@ void launch_classes(Args args, const std::vector<int32_t>& aggs, const std::vect
   }
 }
 
+__global__ void k_dense_eig_warp(int n, const double* a, double* vals, double* vecs, double* ws, int32_t* status) {
+  WarpTeam t;
+  if (threadIdx.x >= 32) return;
+  Arena ar{ws, 0};
+  const int st = t_sym_eig(t, n, a, vals, vecs, ar);
+  if (t.rank() == 0) *status = st;
+}
+
+__global__ void k_dense_eig_block(int n, const double* a, double* vals, double* vecs, double* ws, int32_t* status,
+                                  int use_fast) {
+  BlockTeam t;
+  Arena ar{ws, 0, use_fast ? dyn_smem : nullptr, use_fast ? kFastCap : 0};
+  const int st = t_sym_eig(t, n, a, vals, vecs, ar);
+  if (t.rank() == 0) *status = st;
+}
+
 }  // namespace
+
+int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, int path, cudaStream_t s) {
+  if (getenv("LSB_EIG_PROF")) {
+    static long long* buf = nullptr;
+    if (!buf) LSB_CUDA(cudaMalloc(&buf, 6 * sizeof(long long)));
+    LSB_CUDA(cudaMemset(buf, 0, 6 * sizeof(long long)));
+    LSB_CUDA(cudaMemcpyToSymbol(g_eig_prof, &buf, sizeof(buf)));
+  }
+  DBuf<double> a(n * n, s), vals(std::max<int64_t>(n, 1), s), vecs(std::max<int64_t>(n * n, 1), s),
+      ws(sym_eig_scratch(n) + 64, s);
+  DBuf<int32_t> st(1, s);
+  st.zero(s);
+  a.upload(h_a, n * n, s);
+  if (path == 0) {
+    k_dense_eig_warp<<<1, 32, 0, s>>>(static_cast<int>(n), a.get(), vals.get(), vecs.get(), ws.get(), st.get());
+  } else {
+    const size_t fsm = path == 2 ? size_t(kFastCap) * 8 : 0;
+    LSB_CUDA(cudaFuncSetAttribute(k_dense_eig_block, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFastCap * 8)));
+    k_dense_eig_block<<<1, 512, fsm, s>>>(static_cast<int>(n), a.get(), vals.get(), vecs.get(), ws.get(), st.get(),
+                                          path == 2 ? 1 : 0);
+  }
+  LSB_LAUNCH();
+  const int status = read_scalar(st.get(), s);
+  if (getenv("LSB_EIG_PROF")) {
+    long long* dp = nullptr;
+    LSB_CUDA(cudaMemcpyFromSymbol(&dp, g_eig_prof, sizeof(dp)));
+    if (dp) {
+      long long h[6];
+      LSB_CUDA(cudaMemcpy(h, dp, sizeof(h), cudaMemcpyDeviceToHost));
+      fprintf(stderr, "eig prof (Mcycles): smsum %.1f wait+barrier %.1f params %.1f rotate %.1f rowend %.1f vapply %.1f\n",
+              h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
+    }
+  }
+  const auto hv = vals.download(s);
+  const auto hV = vecs.download(s);
+  std::copy(hv.begin(), hv.begin() + n, h_vals);
+  std::copy(hV.begin(), hV.begin() + n * n, h_vecs);
+  return status;
+}
 
 void row_sets(const DevCsr& g, const DevTopo& topo, DevRowSets& rs, cudaStream_t s) {
   const int64_t m = g.nr, nnz = g.nnz;

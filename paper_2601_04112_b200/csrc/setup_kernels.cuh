@@ -72,6 +72,10 @@ void local_gevp_all(const DevCsr& g, const DevTopo& topo, const std::vector<int3
                     const std::vector<int32_t>& h_gamma_off, const DevRowSets& rs, const std::vector<int64_t>& h_nz_off,
                     const GevpParams& gp, DevInterp& ip, DevCsr& p, bool keep_spectra, cudaStream_t s);
 
+// One dense eigensolve through a chosen device path (0 warp team, 1 CTA
+// team, 2 CTA pipelined); returns 0 or the EigError code. Test hook.
+int dense_sym_eig(int64_t n, const double* a, double* vals, double* vecs, int path, cudaStream_t s);
+
 // Dense Cholesky of the coarsest matrix with the jitter retry, returning the
 // full explicit inverse (row-major) for the coarse solve (hierarchy.hpp:193).
 void coarse_factor(const DevCsr& a, DBuf<double>& inv, cudaStream_t s);

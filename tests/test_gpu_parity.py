@@ -1,0 +1,322 @@
+"""Parity of the CUDA path (through the C ABI) against the plain-C oracle.
+
+Setup is bit-exact: every exported stage of the hierarchy (A_l, G_l, P_l,
+partitions, Γ sets, colours, per-aggregate spectra, row multiplicities)
+must equal the oracle's bits. The solve uses an explicit ω-column inverse
+for the Schwarz blocks and tree reductions for the PCG dots, so it is
+checked with floating-point tolerances: V-cycle ≤ 1e-12 relative, PCG
+iterations within ±1 (north_star), final relative residual ≤ 1e-8.
+"""
+from __future__ import annotations
+
+import threading
+
+import numpy as np
+import pytest
+
+from oracle import refbind
+from paper_2601_04112_b200 import abi, configs, lsamgdd
+
+from . import _cases
+
+pytestmark = pytest.mark.gpu
+
+VCYCLE_RTOL = 1e-12
+SCHWARZ_RTOL = 1e-11
+
+
+def assert_hierarchy_bit_exact(h: lsamgdd.Hierarchy, ho) -> None:
+    assert h.num_levels == ho.num_levels
+    for l in range(ho.num_levels):
+        for w in (abi.EXPORT_A, abi.EXPORT_G):
+            m = h._export_csr(l, w)
+            rp, c, v, shape = ho.export(l, w)
+            assert (m.n_rows, m.n_cols) == shape, (l, w)
+            assert np.array_equal(m.row_offsets, rp) and np.array_equal(m.col_indices, c), (l, w)
+            assert np.array_equal(m.values, v), (l, w)
+        if l + 1 == ho.num_levels:
+            continue
+        m = h._export_csr(l, abi.EXPORT_P)
+        rp, c, v, _ = ho.export(l, abi.EXPORT_P)
+        assert np.array_equal(m.row_offsets, rp) and np.array_equal(m.col_indices, c) and np.array_equal(m.values, v)
+        for w in (abi.EXPORT_PARTITION, abi.EXPORT_COLORS, abi.EXPORT_MULTIPLICITY):
+            a, an = h._export_vec(l, w)
+            b, bn = ho.export(l, w)
+            assert np.array_equal(a, b) and an == bn, (l, w)
+        a0, a1 = h._export_offsets(l, abi.EXPORT_GAMMA)
+        b0, b1 = ho.export(l, abi.EXPORT_GAMMA)
+        assert np.array_equal(a0, b0) and np.array_equal(a1, b1)
+        s0, sv = h._export_offsets(l, abi.EXPORT_SPECTRA, with_vals=True)
+        t0, tv = ho.export(l, abi.EXPORT_SPECTRA)
+        assert np.array_equal(s0, t0) and np.array_equal(sv, tv)
+        sg = h.summary[l]
+        so = ho.summary(l)
+        assert (sg.dim, sg.nnz, sg.n_aggregates, sg.k_c, sg.n_mult, sg.modes_kept) == (
+            so["dim"], so["nnz"], so["n_aggregates"], so["k_c"], so["n_mult"], so["modes_kept"])
+        assert sg.thresh == so["thresh"]
+
+
+CASES = [
+    ("c1", None, {}),
+    ("c2", 64, {}),
+    ("c2", 128, {}),
+    ("c3", 32, {"thresh_override": 0.0}),
+    ("c3", 64, {"thresh_override": 10.0}),
+]
+
+
+@pytest.fixture(scope="module")
+def built():
+    out = {}
+    orc = refbind.oracle()
+    for name, scale, over in CASES:
+        cfg = configs.config(name, scale)
+        h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg, keep_spectra=True, **over))
+        ho = orc.setup(cfg, refbind.params_for(cfg, keep_spectra=1, **over))
+        out[(name, scale)] = (cfg, h, ho)
+    return out
+
+
+@pytest.mark.parametrize("name,scale,over", CASES)
+def test_hierarchy_bit_exact(gpu, built, name, scale, over):
+    cfg, h, ho = built[(name, scale)]
+    assert_hierarchy_bit_exact(h, ho)
+    assert lsamgdd.operator_complexity(h) == ho.operator_complexity()
+
+
+@pytest.mark.parametrize("name,scale,over", CASES)
+def test_vcycle_and_pcg(gpu, built, name, scale, over):
+    cfg, h, ho = built[(name, scale)]
+    r = cfg.rhs
+    e, eo = lsamgdd.vcycle(h, r), ho.vcycle(r)
+    assert np.linalg.norm(e - eo) <= VCYCLE_RTOL * np.linalg.norm(eo)
+    x, rep = lsamgdd.pcg(h, r, 1e-8, 1000)
+    xo, repo = ho.pcg(r, 1e-8, 1000)
+    assert rep.converged and repo["converged"]
+    assert abs(int(rep.iterations) - int(repo["iterations"])) <= 1
+    assert rep.residual_history[-1] <= 1e-8 * rep.residual_history[0]
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
+    assert rep.residual_history.shape[0] == rep.iterations + 1
+    rho = (rep.residual_history[-1] / rep.residual_history[0]) ** (1.0 / rep.iterations)
+    assert rep.avg_conv_factor == pytest.approx(rho, rel=1e-12)
+
+
+@pytest.mark.parametrize("name,scale,over", CASES[:3])
+def test_schwarz_apply(gpu, built, name, scale, over):
+    cfg, h, ho = built[(name, scale)]
+    rng = np.random.default_rng(5)
+    for l in range(h.num_levels - 1):
+        r = rng.uniform(-1, 1, h.summary[l].dim)
+        for mode in (lsamgdd.RAS, lsamgdd.RAST):
+            y = lsamgdd.apply(h, l, r, mode)
+            yo = ho.schwarz_apply(r, l, mode)
+            assert np.linalg.norm(y - yo) <= SCHWARZ_RTOL * np.linalg.norm(yo), (l, mode)
+
+
+@pytest.mark.parametrize("name,scale,over", CASES[:3])
+def test_level_spmv_bit_exact(gpu, built, name, scale, over):
+    cfg, h, ho = built[(name, scale)]
+    rng = np.random.default_rng(6)
+    for l in range(h.num_levels - 1):
+        n = h.summary[l].dim
+        nc = h.summary[l + 1].dim
+        m = h.levels[l].G.n_rows
+        x = rng.uniform(-1, 1, n)
+        assert np.array_equal(lsamgdd.level_spmv(h, l, "A", x), ho.spmv(x, l, 0, False, n))
+        assert np.array_equal(lsamgdd.level_spmv(h, l, "G", x), ho.spmv(x, l, 1, False, m))
+        y = rng.uniform(-1, 1, m)
+        y[::7] = 0.0  # exercises the reference's zero skip (sparse.hpp:131)
+        assert np.array_equal(lsamgdd.level_spmv(h, l, "G", y, transpose=True), ho.spmv(y, l, 1, True, n))
+        xc = rng.uniform(-1, 1, nc)
+        assert np.array_equal(lsamgdd.level_spmv(h, l, "P", xc), ho.spmv(xc, l, 2, False, n))
+        assert np.array_equal(lsamgdd.level_spmv(h, l, "P", x, transpose=True), ho.spmv(x, l, 2, True, nc))
+
+
+def test_reference_generator_default_params(gpu, oracle_lib):
+    """No config hooks: the reference's own rotated-anisotropy generator with
+    default LevelParams (multi-level greedy aggregation, κ threshold)."""
+    g = _cases.rotated_aniso_ref(32, 32, 1e-4, 0.5)
+    h = lsamgdd.setup(g, lsamgdd.LevelParams(coarse_size=20, keep_spectra=True))
+    ho = oracle_lib.setup(g, _cases.params(coarse_size=20, keep_spectra=1))
+    assert h.num_levels >= 3
+    assert_hierarchy_bit_exact(h, ho)
+
+
+def test_two_pass_aggregation(gpu, oracle_lib):
+    """aggregation_passes = 2 (multi_pass_aggregation, aggregation.hpp:138-155)."""
+    g = _cases.rotated_aniso_ref(24, 24, 1e-2, 0.3)
+    h = lsamgdd.setup(g, lsamgdd.LevelParams(coarse_size=20, aggregation_passes=2, coarsening_ratios=(4, 5),
+                                              keep_spectra=True))
+    ho = oracle_lib.setup(g, _cases.params(coarse_size=20, aggregation_passes=2, coarsening_ratios=[4, 5],
+                                           keep_spectra=1))
+    assert_hierarchy_bit_exact(h, ho)
+
+
+def test_weighted_lhs_variant(gpu, oracle_lib):
+    """GevpVariant::WeightedLhs (splitting.hpp:45, :210-212)."""
+    g = _cases.rotated_aniso_ref(20, 20, 1e-3, 0.4)
+    h = lsamgdd.setup(g, lsamgdd.LevelParams(coarse_size=20, gevp_variant=1, keep_spectra=True))
+    ho = oracle_lib.setup(g, _cases.params(coarse_size=20, gevp_variant=1, keep_spectra=1))
+    assert_hierarchy_bit_exact(h, ho)
+
+
+def test_golden_topology_and_multiplicity(gpu):
+    """test_aggregation.cpp:139-156 and test_splitting.cpp:37-58 through the GPU."""
+    g = _cases.chain_factor(9, shift=0.25)
+    h = lsamgdd.setup(g, lsamgdd.LevelParams(max_levels=2, coarse_size=1,
+                                              level0_partition=np.array([0, 0, 0, 1, 1, 1, 2, 2, 2]),
+                                              level0_n_aggregates=3))
+    t = h.levels[0].topology
+    assert [x.tolist() for x in t.gamma] == [[3], [2, 6], [5]]
+    assert t.n_colors == 2
+    assert t.subdomain(1).tolist() == [3, 4, 5, 2, 6]
+    assert t.pou_mask(1).tolist() == [1, 1, 1, 0, 0]
+    g6 = _cases.chain_factor(6)
+    h6 = lsamgdd.setup(g6, lsamgdd.LevelParams(max_levels=2, coarse_size=1,
+                                                level0_partition=np.array([0, 0, 0, 1, 1, 1]), level0_n_aggregates=2))
+    assert h6.levels[0].multiplicity().tolist() == [1, 1, 2, 1, 1]
+
+
+def test_smoother_dense_reference(gpu):
+    """test_smoother.cpp:79-107 through the GPU: RAS / RAS-T vs dense inverses."""
+    g = _cases.chain_factor(12, shift=0.5)
+    part = np.array([0, 0, 0, 0, 1, 1, 1, 2, 2, 2, 2, 2])
+    h = lsamgdd.setup(g, lsamgdd.LevelParams(max_levels=2, coarse_size=1, level0_partition=part, level0_n_aggregates=3))
+    A = h.levels[0].A.todense()
+    t = h.levels[0].topology
+    n = 12
+    for mode in (lsamgdd.RAS, lsamgdd.RAST):
+        want = np.zeros((n, n))
+        for i in range(3):
+            om, sub = t.omega[i].tolist(), t.subdomain(i).tolist()
+            inv = np.linalg.inv(A[np.ix_(sub, sub)])
+            for a in range(len(sub)):
+                for b in range(len(sub)):
+                    w = inv[a, b]
+                    if (mode == lsamgdd.RAS and a >= len(om)) or (mode == lsamgdd.RAST and b >= len(om)):
+                        w = 0.0
+                    want[sub[a], sub[b]] += w
+        got = np.stack([lsamgdd.apply(h, 0, np.eye(n)[j], mode) for j in range(n)], axis=1)
+        assert np.linalg.norm(got - want) / np.linalg.norm(want) < 1e-12
+
+
+def test_ras_adjointness(gpu):
+    """acceptance.cpp:178-206: <y, RAS x> = <RAS-T y, x>."""
+    cfg = configs.config("c2", 64)
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg))
+    rng = np.random.default_rng(2024)
+    for _ in range(10):
+        x, y = rng.uniform(-1, 1, cfg.n), rng.uniform(-1, 1, cfg.n)
+        a = y @ lsamgdd.apply(h, 0, x, lsamgdd.RAS)
+        b = lsamgdd.apply(h, 0, y, lsamgdd.RAST) @ x
+        assert abs(a - b) <= 1e-12 * max(abs(a), abs(b))
+
+
+def test_vcycle_symmetric_positive(gpu):
+    """test_hierarchy.cpp:164-182 / acceptance check 4."""
+    cfg = configs.config("c2", 64)
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg))
+    rng = np.random.default_rng(101)
+    for _ in range(10):
+        x, y = rng.uniform(-1, 1, cfg.n), rng.uniform(-1, 1, cfg.n)
+        bx, by = lsamgdd.vcycle(h, x), lsamgdd.vcycle(h, y)
+        scale = np.linalg.norm(y) * np.linalg.norm(bx) + np.linalg.norm(x) * np.linalg.norm(by)
+        assert abs(y @ bx - x @ by) <= 1e-10 * scale
+        assert x @ bx > 0
+
+
+def test_indefinite_parity(gpu, oracle_lib):
+    """Config 3 with the literal threshold 20 makes the cycle indefinite in the
+    reference; the GPU path must raise the same IndefiniteError."""
+    cfg = configs.config("c3", 64)
+    ho = oracle_lib.setup(cfg, refbind.params_for(cfg))
+    with pytest.raises(abi.LsamgddError) as e:
+        ho.pcg(cfg.rhs)
+    assert e.value.name == "IndefiniteError"
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg))
+    with pytest.raises(lsamgdd.IndefiniteError):
+        lsamgdd.pcg(h, cfg.rhs)
+
+
+def test_stagnation_is_setup_error(gpu):
+    """test_hierarchy.cpp:180-187: an identity factor cannot coarsen."""
+    g = _cases.csr_from_dense(np.eye(30)) + (30,)
+    with pytest.raises(lsamgdd.SetupError):
+        lsamgdd.setup(g, lsamgdd.LevelParams(coarse_size=10))
+
+
+def test_pcg_contracts_gpu(gpu):
+    cfg = configs.config("c2", 32)
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg))
+    x, rep = lsamgdd.pcg(h, np.zeros(cfg.n))
+    assert rep.converged and rep.iterations == 0 and not x.any()
+    x, rep = lsamgdd.pcg(h, cfg.rhs, 1e-14, 2)
+    assert not rep.converged and rep.iterations == 2
+
+
+def test_deterministic_and_reentrant(gpu):
+    """Bit-identical reruns; concurrent solves on one immutable handle
+    (hierarchy.hpp:56-57)."""
+    cfg = configs.config("c2", 64)
+    p = lsamgdd.params_for(cfg)
+    h1, h2 = lsamgdd.setup(cfg, p), lsamgdd.setup(cfg, p)
+    x1, _ = lsamgdd.pcg(h1, cfg.rhs)
+    x2, _ = lsamgdd.pcg(h2, cfg.rhs)
+    assert np.array_equal(x1, x2)
+    outs = [None] * 4
+    rhs = [configs.mt19937_64_uniform(10 + i, cfg.n) for i in range(4)]
+
+    def work(i):
+        outs[i] = lsamgdd.pcg(h1, rhs[i])[0]
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(4)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(4):
+        assert np.array_equal(outs[i], lsamgdd.pcg(h1, rhs[i])[0])
+
+
+def test_full_size_config2(gpu):
+    """BASELINE config 2 at full size (1024², n = 1,048,576): size-independent
+    properties — convergence to 1e-8, a symmetric positive cycle, P panels
+    orthonormal (PᵀP = I, test_hierarchy.cpp:98-101) and determinism."""
+    cfg = configs.config("c2")
+    p = lsamgdd.params_for(cfg)
+    h = lsamgdd.setup(cfg, p)
+    x, rep = lsamgdd.pcg(h, cfg.rhs, 1e-8, 1000)
+    assert rep.converged and rep.residual_history[-1] <= 1e-8 * rep.residual_history[0]
+    rng = np.random.default_rng(3)
+    a, b = rng.uniform(-1, 1, cfg.n), rng.uniform(-1, 1, cfg.n)
+    ba, bb = lsamgdd.vcycle(h, a), lsamgdd.vcycle(h, b)
+    assert abs(b @ ba - a @ bb) <= 1e-10 * (np.linalg.norm(b) * np.linalg.norm(ba) + np.linalg.norm(a) * np.linalg.norm(bb))
+    P = h.levels[0].P
+    # PᵀP = I column-block by column-block: Σ_rows P(r,i) P(r,j)
+    rows = np.repeat(np.arange(P.n_rows), np.diff(P.row_offsets))
+    cols = P.col_indices
+    diag = np.zeros(P.n_cols)
+    np.add.at(diag, cols, P.values ** 2)
+    assert np.abs(diag - 1.0).max() < 1e-12
+    assert rows.shape[0] == P.nnz
+    x2, _ = lsamgdd.pcg(h, cfg.rhs, 1e-8, 1000)
+    assert np.array_equal(x, x2)
+
+
+@pytest.mark.parametrize("n,path", [(7, 0), (30, 0), (30, 1), (64, 1), (64, 2), (150, 2), (333, 2)])
+def test_dense_eigensolver_paths_bit_exact(gpu, oracle_lib, n, path):
+    """Each device path of the batched Jacobi (warp team, CTA team, CTA
+    pipelined with TMA-prefetched rows) equals eigen.hpp:35-118 bit for bit."""
+    import ctypes as C
+    rng = np.random.default_rng(n + 17 * path)
+    a = rng.uniform(-1, 1, (n, n))
+    a[np.abs(a) < 0.3] = 0.0  # some exact zeros, like the Gram blocks
+    a = a @ a.T  # SPSD
+    vals, vecs = oracle_lib.sym_eig(a)
+    gv, gV = np.empty(n), np.empty((n, n))
+    err = C.create_string_buffer(512)
+    st = lsamgdd.library().lsamgdd_dense_sym_eig(C.c_int64(n), abi.ptr(np.ascontiguousarray(a)), abi.ptr(gv),
+                                                 abi.ptr(gV), C.c_int32(path), err, C.c_size_t(512))
+    assert st == 0, err.value
+    assert np.array_equal(gv, vals)
+    assert np.array_equal(gV, vecs)
