@@ -37,7 +37,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "AMG-DD setup+PCG solve unknowns/s"
 UNIT = "unknowns/s"
-SAMPLE_GRID = 256  # bounded CPU sample of config 2 (same generator and parameters)
+SAMPLE_GRID = 384  # bounded CPU sample of config 2 (same generator and parameters, ~30 s single-threaded)
 
 
 def env_int(k, d):

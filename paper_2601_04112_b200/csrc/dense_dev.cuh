@@ -12,6 +12,7 @@
 //     touches rows/columns p and q only), two team barriers per rotation.
 #pragma once
 
+#include <cuda/atomic>
 #include <type_traits>
 
 #include "common.cuh"
@@ -294,8 +295,374 @@ __device__ int cta_sym_eig_pipelined(int n, const double* m, double* vals, doubl
   return 0;
 }
 
-__device__ inline int cta_sym_eig_pipelined_any(int n, const double* m, double* vals, double* vecs, double* A,
+// ---- producer/consumer variant --------------------------------------------------------
+//
+// Same arithmetic and sequence as cta_sym_eig_pipelined. Warp 0 (producer)
+// runs only the sequential chain: for rotation (p,q) it applies rotation
+// (p,q-1) to pair j = q, computes (s, tau, h) of rotation (p,q), updates d/z
+// and publishes. Warps 1..15 (consumers) apply each published rotation to all
+// other pairs (j ∉ {p, q, q+1}) and to Vᵀ one or two rotations behind, keep
+// the cp.async ring of partner rows full, and meet at a named barrier. To keep
+// the consumers off the L1/LSU limit:
+//   * a(p,j) and v(j,p) live in the owner thread's registers for the whole row
+//     (thread j mod 480 owns pair j); the producer receives a(p,q+1) through a
+//     shared hand-off slot and returns the pivot's final value in the queue;
+//   * patches of in-flight rows are direct-mapped by rotation distance;
+//   * mirrored-column stores of rotations (2k, 2k+1) go out as one 16-byte
+//     store during rotation 2k+1 (still inside the patch window).
+constexpr int kMaxOwn = 5;  // pairs per consumer thread: n <= 384 * kMaxOwn
+
+template <int R>
+__device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs, double* A, double* Vt, double* sm) {
+  // Warp 0 (SMSP 0) produces; warps 4, 8, 12 idle so SMSP 0 issues only the
+  // producer's dependent chain; the other 12 warps consume.
+  constexpr int D = R - 2, NL = 2 * R, PS = R + 1, T = kPipeThreads, NC = 384, QN = 64;
+  const int tid = threadIdx.x;
+  const int wid = tid >> 5;
+  const bool producer = wid == 0;
+  const bool idle = (wid & 3) == 0 && wid != 0;
+  const int ctid = (wid - 1 - (wid >> 2)) * 32 + (tid & 31);  // consumer index 0..383
+  const int64_t ld = (n + 1) & ~int64_t(1);
+  double* pvs = sm;                      // a(p,·) at row start / hand-offs
+  double* vp = pvs + ld;                 // Vᵀ row p at row start
+  double* ring = vp + ld;
+  double* d = ring + int64_t(2 * R) * ld;
+  double* bb = d + ld;
+  double* z = bb + ld;
+  double* slot = z + ld;
+  double* patch = slot + 16;             // [NL][R+1] by rotation distance 1..R
+  __shared__ unsigned pmask[NL];
+  __shared__ double q_s[QN], q_tau[QN], q_piv[QN], q_ny[QN];
+  __shared__ int q_rot[QN];
+  for (int64_t e = tid; e < int64_t(n) * n; e += T) {  // full symmetric copy (eigen.hpp:44)
+    const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
+    double val = m[e];
+    if (i != j) {
+      const int lo = i < j ? i : j, hi = i < j ? j : i;
+      val = 0.5 * (m[int64_t(lo) * n + hi] + m[int64_t(hi) * n + lo]);
+    }
+    A[int64_t(i) * ld + j] = val;
+    Vt[int64_t(i) * ld + j] = (i == j) ? 1.0 : 0.0;
+  }
+  for (int i = tid; i < n; i += T) {
+    d[i] = bb[i] = m[int64_t(i) * n + i];
+    z[i] = 0.0;
+  }
+  __syncthreads();
+  const int chunks = static_cast<int>(ld / 2);
+  auto prefetch = [&](int row) {  // consumers only
+    if (row < n) {
+      double* dst = ring + int64_t(2 * (row % R)) * ld;
+      const double* srca = A + int64_t(row) * ld;
+      const double* srcv = Vt + int64_t(row) * ld;
+      for (int c = ctid; c < chunks; c += NC) {
+        cp_async16(dst + 2 * c, srca + 2 * c);
+        cp_async16(dst + ld + 2 * c, srcv + 2 * c);
+      }
+    }
+    cp_async_commit();
+  };
+  // Round q of the rotation barrier: the consumers have finished rotation q-1
+  // and landed row q; the producer has published rotation q.
+  auto rbar = []() { asm volatile("bar.sync 1, %0;" ::"n"(NC + 32) : "memory"); };
+  long long base = 0;
+  bool converged = false;
+  long long* const prof = g_eig_prof;  // optional cycle counters (test hook)
+  long long c_w = 0, c_c = 0, c_b = 0, c_p = 0, c_r = 0, c_e = 0, c_n = 0;
+  for (int sweep = 0; sweep < 64; ++sweep) {
+    double smv = 0.0;
+    for (int p = 0; p + 1 < n; ++p) {
+      for (int q = p + 1 + tid; q < n; q += T) ring[q] = A[int64_t(p) * ld + q];
+      __syncthreads();
+      if (tid == 0)
+        for (int q = p + 1; q < n; ++q) smv += fabs(ring[q]);
+      __syncthreads();
+    }
+    if (tid == 0) slot[0] = smv;
+    __syncthreads();
+    smv = slot[0];
+    if (smv == 0.0) {
+      converged = true;
+      break;
+    }
+    const double tresh = sweep < 3 ? 0.2 * smv / static_cast<double>(static_cast<uint64_t>(n) * n) : 0.0;
+    for (int p = 0; p + 1 < n; ++p) {
+      for (int j = tid; j < n; j += T) {
+        pvs[j] = A[int64_t(p) * ld + j];
+        vp[j] = Vt[int64_t(p) * ld + j];
+      }
+      if (tid < NL) pmask[tid] = 0u;
+      __syncthreads();
+      if (producer) {
+        // all 32 lanes walk the rounds (bar.sync is warp-aligned); lane 0 computes
+        double dp = d[p], zp = z[p];
+        double ps = 0.0, ptau = 0.0, ph = 0.0;
+        int prot = 0;
+        double ny_prev = 0.0;
+        for (int q = p + 1; q < n; ++q) {
+          const long long t = base + (q - p - 1);
+          const long long k1 = prof ? clock64() : 0;
+          if (tid == 0) {
+            double apq = pvs[q];  // a(p,q) after the consumers' rotations <= q-2 (hand-off)
+            if (q > p + 1) {
+              if (prot) {  // rotation q-1 on pair q; the owner of q-1 stores a(q-1,q) at rotation q
+                const int pq = q - 1;
+                const double hy = ring[int64_t(2 * (pq % R)) * ld + q];
+                const double gx = apq;
+                ny_prev = hy + ps * (gx - hy * ptau);
+                apq = gx - ps * (hy + gx * ptau);
+                z[pq] += ph;
+                d[pq] += ph;
+              }
+            }
+            const double dq = d[q];
+            const double g = 100.0 * fabs(apq);
+            double s = 0.0, tau = 0.0, h = 0.0;
+            int rot = 0, zero = 0;
+            if (sweep > 3 && fabs(dp) + g == fabs(dp) && fabs(dq) + g == fabs(dq)) {
+              zero = 1;
+            } else if (fabs(apq) > tresh) {
+              double hh = dq - dp;
+              double tt;
+              if (fabs(hh) + g == fabs(hh)) {
+                tt = apq / hh;
+              } else {
+                const double theta = 0.5 * hh / apq;
+                tt = 1.0 / (fabs(theta) + sqrt(1.0 + theta * theta));
+                if (theta < 0.0) tt = -tt;
+              }
+              const double c = 1.0 / sqrt(1.0 + tt * tt);
+              s = tt * c;
+              tau = s / (1.0 + c);
+              h = tt * apq;
+              zp -= h;
+              dp -= h;
+              zero = 1;
+              rot = 1;
+            }
+            const int qi = static_cast<int>(t % QN);
+            q_s[qi] = s;
+            q_tau[qi] = tau;
+            q_rot[qi] = rot;
+            q_piv[qi] = zero ? 0.0 : apq;  // a(p,q) after rotation q (pair q resumes at q+1)
+            q_ny[qi] = ny_prev;            // a(q,q-1) after rotation q-1 (valid when rotation q-1 rotated)
+            ps = s;
+            ptau = tau;
+            ph = h;
+            prot = rot;
+          }
+          __syncwarp();
+          const long long k2 = prof ? clock64() : 0;
+          rbar();  // round q: publish rotation q; rotation q-1 done, row q landed
+          if (prof) {
+            c_c += k2 - k1;
+            c_w += clock64() - k2;
+            ++c_n;
+          }
+        }
+        if (tid == 0) {
+          if (prot) {  // the row's last rotation: its diagonal updates
+            z[n - 1] += ph;
+            d[n - 1] += ph;
+          }
+          d[p] = dp;
+          z[p] = zp;
+        }
+      } else if (!idle) {
+        // owner registers: pair j = ctid + k*NC
+        double pr[kMaxOwn], vr[kMaxOwn], pend[kMaxOwn];
+#pragma unroll
+        for (int k = 0; k < kMaxOwn; ++k) {
+          const int j = ctid + k * NC;
+          pr[k] = j < n ? pvs[j] : 0.0;
+          vr[k] = j < n ? vp[j] : 0.0;
+          pend[k] = 0.0;
+        }
+        int pend_q = -1;  // rotation whose mirror stores are held back
+        for (int k = 1; k <= D; ++k) prefetch(p + k);
+        for (int q = p + 1; q < n; ++q) {
+          const long long t = base + (q - p - 1);
+          const long long k0 = prof ? clock64() : 0;
+          prefetch(q + D);
+          cp_async_wait<D>();
+          const long long k1 = prof ? clock64() : 0;
+          rbar();  // round q
+          const long long k2 = prof ? clock64() : 0;
+          if (ctid == 0) pmask[(q + R + 1) % NL] = 0u;  // before any rotation can patch row q+R+1
+          const int qi = static_cast<int>(t % QN);
+          const int qp = static_cast<int>((t + QN - 1) % QN);  // rotation q-1 (when q-1 > p)
+          const bool rot = q_rot[qi] != 0;
+          const double s = q_s[qi], tau = q_tau[qi];
+          const double* qv = ring + int64_t(2 * (q % R)) * ld;
+          const double* qvv = qv + ld;
+          double* const arow = A + int64_t(q) * ld;
+          double* const vrow = Vt + int64_t(q) * ld;
+          const bool pair_odd = (q & 1) != 0;
+          const bool held_q = pend_q == q - 1;
+#pragma unroll
+          for (int k = 0; k < kMaxOwn; ++k) {
+            const int j = ctid + k * NC;
+            if (j >= n) break;
+            double* const mir = A + int64_t(j) * ld;  // row j: mirrored column entries
+            if (static_cast<unsigned>(j - q + R) > static_cast<unsigned>(2 * R) && j != p) {
+              // fast path: not excluded, no patch to read or write, no hand-off
+              if (rot) {
+                const double vx = vr[k], vy = qvv[j];
+                vr[k] = vx - s * (vy + vx * tau);
+                vrow[j] = vy + s * (vx - vy * tau);
+                const double hy = qv[j], gx = pr[k];
+                const double ny = hy + s * (gx - hy * tau);
+                pr[k] = gx - s * (hy + gx * tau);
+                arow[j] = ny;
+                if (held_q) {  // rotations (q-1, q): one 16-byte store, q-1 even, ld even
+                  double2 v2;
+                  v2.x = pend[k];
+                  v2.y = ny;
+                  *reinterpret_cast<double2*>(mir + q - 1) = v2;
+                } else if (pair_odd) {
+                  mir[q] = ny;
+                } else {
+                  pend[k] = ny;  // held until rotation q+1
+                }
+              } else if (held_q) {
+                mir[q - 1] = pend[k];
+              }
+              continue;
+            }
+            if (j == q - 1 && j > p) pr[k] = q_piv[qp];  // the pivot of rotation q-1 resumes
+            const bool held = held_q && j != p && j != q - 1 && j != q;
+            if (rot) {
+              const double vx = vr[k], vy = qvv[j];
+              vr[k] = vx - s * (vy + vx * tau);
+              vrow[j] = vy + s * (vx - vy * tau);
+            }
+            const bool prev_rot = j == q - 1 && j > p && q_rot[qp] != 0;  // a(q,q-1) from the producer
+            if (!rot || j == p || j == q || j == q + 1) {
+              if (held) mir[q - 1] = pend[k];
+              if (prev_rot) {
+                arow[j] = q_ny[qi];
+                mir[q] = q_ny[qi];
+              }
+            } else {
+              const int lr = q % NL;
+              double hy = qv[j];
+              const int dist = q - j;
+              if (prev_rot) {
+                hy = q_ny[qi];
+              } else if (dist >= 2 && dist <= R && ((pmask[lr] >> dist) & 1u)) {
+                hy = patch[lr * PS + dist];
+              }
+              const double gx = pr[k];
+              const double ny = hy + s * (gx - hy * tau);
+              pr[k] = gx - s * (hy + gx * tau);
+              arow[j] = ny;
+              if (held) {
+                double2 v2;
+                v2.x = pend[k];
+                v2.y = ny;
+                *reinterpret_cast<double2*>(mir + q - 1) = v2;
+              } else if (pair_odd) {
+                mir[q] = ny;
+              } else {
+                pend[k] = ny;
+              }
+              // rows up to q+R may have been fetched before this rotation's mirror
+              // store (held one rotation) becomes visible
+              if (j > q + 1 && j <= q + R) {
+                const int lj = j % NL;
+                patch[lj * PS + (j - q)] = ny;
+                atomicOr(&pmask[lj], 1u << (j - q));
+              }
+            }
+            if (j == q + 2) pvs[j] = pr[k];  // hand-off: the producer applies rotation q+1
+          }
+          if (rot && !pair_odd)
+            pend_q = q;
+          else
+            pend_q = -1;
+          if (prof) {
+            const long long k3 = clock64();
+            c_b += k1 - k0;
+            c_p += k2 - k1;
+            c_r += k3 - k2;
+          }
+        }
+        cp_async_wait<0>();
+        // flush a mirror still held from the row's last even rotation
+        if (pend_q >= 0) {
+#pragma unroll
+          for (int k = 0; k < kMaxOwn; ++k) {
+            const int j = ctid + k * NC;
+            if (j < n && j != p && j != pend_q && j != pend_q + 1) A[int64_t(j) * ld + pend_q] = pend[k];
+          }
+        }
+        const double piv_last = q_piv[(base + (n - 1 - p - 1)) % QN];  // the last pivot's final value
+#pragma unroll
+        for (int k = 0; k < kMaxOwn; ++k) {
+          const int j = ctid + k * NC;
+          if (j < n) {
+            pvs[j] = (j == n - 1 && j > p) ? piv_last : pr[k];
+            vp[j] = vr[k];
+          }
+        }
+      }
+      base += n - p - 1;
+      const long long k4 = prof ? clock64() : 0;
+      __syncthreads();
+      for (int j = tid; j < n; j += T) {
+        Vt[int64_t(p) * ld + j] = vp[j];
+        if (j == p) continue;
+        A[int64_t(p) * ld + j] = pvs[j];
+        A[int64_t(j) * ld + p] = pvs[j];
+      }
+      __syncthreads();
+      if (prof) c_e += clock64() - k4;
+    }
+    for (int i = tid; i < n; i += T) {
+      bb[i] += z[i];
+      d[i] = bb[i];
+      z[i] = 0.0;
+    }
+    __syncthreads();
+  }
+  if (prof) {
+    if (tid == 0) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[0]), c_w);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[1]), c_c);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[5]), c_e);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[6]), c_n);
+    }
+    if (tid == 32) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[2]), c_b);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[3]), c_p);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[4]), c_r);
+    }
+  }
+  if (!converged) return 1;
+  for (int i = 0; i < n; ++i)
+    if (!isfinite(d[i])) return 2;
+  for (int k = tid; k < n; k += T) {
+    const double dk = d[k];
+    int pos = 0;
+    for (int i = 0; i < n; ++i)
+      if (d[i] < dk || (d[i] == dk && i < k)) ++pos;
+    vals[pos] = dk;
+    for (int i = 0; i < n; ++i) vecs[int64_t(i) * n + pos] = Vt[int64_t(k) * ld + i];
+  }
+  __syncthreads();
+  return 0;
+}
+
+__device__ int g_eig_split = 1;
+  // 1: producer/consumer, 0: one barrier per rotation (test hook)
+
+__device__ __noinline__ int cta_sym_eig_pipelined_any(int n, const double* m, double* vals, double* vecs, double* A,
                                                 double* Vt, double* sm, int R) {
+  if (g_eig_split && n <= 384 * kMaxOwn) {
+    if (R >= 8) return cta_sym_eig_pc<8>(n, m, vals, vecs, A, Vt, sm);
+    if (R >= 6) return cta_sym_eig_pc<6>(n, m, vals, vecs, A, Vt, sm);
+    return cta_sym_eig_pc<4>(n, m, vals, vecs, A, Vt, sm);
+  }
   if (R >= 8) return cta_sym_eig_pipelined<8>(n, m, vals, vecs, A, Vt, sm);
   if (R >= 6) return cta_sym_eig_pipelined<6>(n, m, vals, vecs, A, Vt, sm);
   return cta_sym_eig_pipelined<4>(n, m, vals, vecs, A, Vt, sm);

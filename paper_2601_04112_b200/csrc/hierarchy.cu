@@ -298,6 +298,15 @@ SchwarzView Level::schwarz_view() const {
   v.order = sm.order.get();
   v.max_omega = sm.max_omega;
   v.max_sub = sm.max_sub;
+  v.n_groups = sm.n_groups;
+  v.g_nw = sm.g_nw.get();
+  v.g_ng = sm.g_ng.get();
+  v.g_cnt = sm.g_cnt.get();
+  v.g_ids_off = sm.g_ids_off.get();
+  v.g_blk_off = sm.g_blk_off.get();
+  v.lane_ids = sm.lane_ids.get();
+  v.lane_blk = sm.lane_blk.get();
+  v.color_goff = &sm.color_goff;
   return v;
 }
 
@@ -608,7 +617,7 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
     *stats = lsamgdd_kernel_stats{};
     stats->schwarz_ms = sw_ms;
     stats->schwarz_bytes = static_cast<double>(graph_launches) * (h.levels.size() > 1 ? h.levels[0].sm.bytes_ras + h.levels[0].sm.bytes_rast : 0.0);
-    stats->schwarz_launches = graph_launches * (h.levels.size() > 1 ? 1 + static_cast<int64_t>(h.levels[0].sm.color_off.size()) - 1 : 0);
+    stats->schwarz_launches = graph_launches * (h.levels.size() > 1 ? static_cast<int64_t>(h.levels[0].sm.color_off.size()) : 0);
     stats->total_launches = out.launches;
   }
   return out;

@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <numeric>
+#include <tuple>
 #include <cstdio>
 #include <cstdlib>
 
@@ -321,7 +322,7 @@ __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
 constexpr int64_t kFastCap = 24 * 1024;  // shared doubles for the pipelined Jacobi (192 KiB)
 
 template <bool SMEM>
-__global__ void k_gevp_block(GevpArgs g) {
+__global__ void __launch_bounds__(512) k_gevp_block(GevpArgs g) {
   BlockTeam t;
   double* ws = SMEM ? dyn_smem : g.gws + int64_t(blockIdx.x) * g.ws_stride;
   for (int idx = blockIdx.x; idx < g.n_list; idx += gridDim.x) {
@@ -481,6 +482,76 @@ __global__ void k_sm_block(SmArgs g) {
   for (int idx = blockIdx.x; idx < g.n_list; idx += gridDim.x) smoother_problem(t, g, idx, ws);
 }
 
+// ---- lane-interleaved Schwarz layout ------------------------------------------------
+
+__global__ void k_lane_pack(const int32_t* g_agg, const int32_t* g_nw, const int32_t* g_ng, const int64_t* g_ids_off,
+                            const int64_t* g_blk_off, int64_t n_groups, const int32_t* omega_off, const int32_t* omega,
+                            const int32_t* gamma_off, const int32_t* gamma, const int64_t* sm_off, const double* sm_data,
+                            int32_t* lane_ids, double* lane_blk) {
+  const int lane = threadIdx.x & 31;
+  for (int64_t g = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); g < n_groups;
+       g += int64_t(gridDim.x) * (blockDim.x >> 5)) {
+    const int a = g_agg[g * 32 + lane];
+    const int nw = g_nw[g], ng = g_ng[g];
+    const int m = nw + ng;
+    const int64_t nblk = int64_t(nw) * (nw + 1) / 2 + int64_t(nw) * ng;
+    int32_t* ids = lane_ids + g_ids_off[g];
+    double* blk = lane_blk + g_blk_off[g];
+    for (int e = 0; e < m; ++e) {
+      int id = -1;
+      if (a >= 0) id = e < nw ? omega[omega_off[a] + e] : gamma[gamma_off[a] + e - nw];
+      ids[e * 32 + lane] = id;
+    }
+    for (int64_t k = 0; k < nblk; ++k) blk[k * 32 + lane] = a >= 0 ? sm_data[sm_off[a] + k] : 0.0;
+  }
+}
+
+void build_lane_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, const std::vector<int32_t>& hgo,
+                       const std::vector<int64_t>& colors, int64_t n_colors, DevSmoother& sm, cudaStream_t s) {
+  const int64_t na = topo.n_agg;
+  // groups: (colour, nω, nΓ) keys in colour order, aggregates ascending inside a key
+  std::vector<int64_t> order(na);
+  std::iota(order.begin(), order.end(), 0);
+  auto key = [&](int64_t a) {
+    return std::make_tuple(colors[a], hoo[a + 1] - hoo[a], hgo[a + 1] - hgo[a]);
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int64_t x, int64_t y) { return key(x) < key(y); });
+  std::vector<int32_t> g_agg, g_nw, g_ng, g_cnt;
+  std::vector<int64_t> g_ids_off{0}, g_blk_off{0};
+  sm.color_goff.assign(n_colors + 1, 0);
+  size_t i = 0;
+  while (i < order.size()) {
+    const auto k = key(order[i]);
+    size_t j = i;
+    while (j < order.size() && j - i < 32 && key(order[j]) == k) ++j;
+    const int nw = std::get<1>(k), ng = std::get<2>(k);
+    for (size_t t = i; t < i + 32; ++t) g_agg.push_back(t < j ? static_cast<int32_t>(order[t]) : -1);
+    g_nw.push_back(nw);
+    g_ng.push_back(ng);
+    g_cnt.push_back(static_cast<int32_t>(j - i));
+    g_ids_off.push_back(g_ids_off.back() + int64_t(nw + ng) * 32);
+    g_blk_off.push_back(g_blk_off.back() + (int64_t(nw) * (nw + 1) / 2 + int64_t(nw) * ng) * 32);
+    ++sm.color_goff[std::get<0>(k) + 1];
+    i = j;
+  }
+  for (int64_t c = 0; c < n_colors; ++c) sm.color_goff[c + 1] += sm.color_goff[c];
+  sm.n_groups = static_cast<int64_t>(g_nw.size());
+  DBuf<int32_t> d_agg;
+  d_agg.upload(g_agg, s);
+  sm.g_nw.upload(g_nw, s);
+  sm.g_ng.upload(g_ng, s);
+  sm.g_cnt.upload(g_cnt, s);
+  sm.g_ids_off.upload(g_ids_off, s);
+  sm.g_blk_off.upload(g_blk_off, s);
+  sm.lane_ids.alloc(std::max<int64_t>(g_ids_off.back(), 1), s);
+  sm.lane_blk.alloc(std::max<int64_t>(g_blk_off.back(), 1), s);
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(sm.n_groups, 8), sm_count() * 8)));
+  k_lane_pack<<<grid, 256, 0, s>>>(d_agg.get(), sm.g_nw.get(), sm.g_ng.get(), sm.g_ids_off.get(), sm.g_blk_off.get(),
+                                   sm.n_groups, topo.omega_off.get(), topo.omega.get(), topo.gamma_off.get(),
+                                   topo.gamma.get(), sm.off.get(), sm.data.get(), sm.lane_ids.get(), sm.lane_blk.get());
+  LSB_LAUNCH();
+}
+
 // ---- coarse factor -------------------------------------------------------------
 
 __global__ void k_coarse_dense(const int64_t* off, const int32_t* col, const double* val, int64_t n, double* d) {
@@ -605,7 +676,7 @@ __global__ void k_dense_eig_warp(int n, const double* a, double* vals, double* v
   if (t.rank() == 0) *status = st;
 }
 
-__global__ void k_dense_eig_block(int n, const double* a, double* vals, double* vecs, double* ws, int32_t* status,
+__global__ void __launch_bounds__(512) k_dense_eig_block(int n, const double* a, double* vals, double* vecs, double* ws, int32_t* status,
                                   int use_fast) {
   BlockTeam t;
   Arena ar{ws, 0, use_fast ? dyn_smem : nullptr, use_fast ? kFastCap : 0};
@@ -616,10 +687,15 @@ __global__ void k_dense_eig_block(int n, const double* a, double* vals, double* 
 }  // namespace
 
 int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, int path, cudaStream_t s) {
+  {
+    const char* e = getenv("LSB_EIG_SPLIT");
+    const int split = (e && e[0] == '0') ? 0 : 1;
+    LSB_CUDA(cudaMemcpyToSymbol(g_eig_split, &split, sizeof(split)));
+  }
   if (getenv("LSB_EIG_PROF")) {
     static long long* buf = nullptr;
-    if (!buf) LSB_CUDA(cudaMalloc(&buf, 6 * sizeof(long long)));
-    LSB_CUDA(cudaMemset(buf, 0, 6 * sizeof(long long)));
+    if (!buf) LSB_CUDA(cudaMalloc(&buf, 8 * sizeof(long long)));
+    LSB_CUDA(cudaMemset(buf, 0, 8 * sizeof(long long)));
     LSB_CUDA(cudaMemcpyToSymbol(g_eig_prof, &buf, sizeof(buf)));
   }
   DBuf<double> a(n * n, s), vals(std::max<int64_t>(n, 1), s), vecs(std::max<int64_t>(n * n, 1), s),
@@ -641,10 +717,10 @@ int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, 
     long long* dp = nullptr;
     LSB_CUDA(cudaMemcpyFromSymbol(&dp, g_eig_prof, sizeof(dp)));
     if (dp) {
-      long long h[6];
+      long long h[8];
       LSB_CUDA(cudaMemcpy(h, dp, sizeof(h), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "eig prof (Mcycles): smsum %.1f wait+barrier %.1f params %.1f rotate %.1f rowend %.1f vapply %.1f\n",
-              h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6);
+      fprintf(stderr, "eig prof (Mcycles): [pipelined: smsum wait+barrier params rotate rowend vapply | p/c: prod-barrier prod-chain cons-prefetch cons-barrier cons-rotate rowend] %.1f %.1f %.1f %.1f %.1f %.1f rotations %lld\n",
+              h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6, h[6]);
     }
   }
   const auto hv = vals.download(s);
@@ -748,6 +824,8 @@ void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int3
   for (int64_t i = 0; i < na; ++i)
     if (hs[i]) raise(LSAMGDD_ERR_SETUP, "dense symmetric factorization failed for subdomain block of aggregate " +
                                             std::to_string(i));
+  if (sm.max_sub <= kLaneMaxSub && sm.max_omega <= kLaneMaxOmega)
+    build_lane_layout(topo, hoo, hgo, colors, n_colors, sm, s);
   // colour-sorted aggregate order for the race-free RAS-T scatter
   std::vector<int32_t> byc(na);
   sm.color_off.assign(n_colors + 1, 0);

@@ -38,7 +38,19 @@ struct DevSmoother {
   std::vector<int64_t> color_off;  // host, n_colors + 1
   int64_t max_omega = 0, max_sub = 0;
   double bytes_ras = 0, bytes_rast = 0;  // algorithmic bytes per sweep
+  // Lane-interleaved layout for small subdomains (nΩ <= kLaneMaxSub): groups
+  // of up to 32 aggregates with one (colour, nω, nΓ) shape; element e of lane
+  // l lives at [e][l], so every warp load is one 256-byte transaction.
+  int64_t n_groups = 0;
+  DBuf<int32_t> g_nw, g_ng, g_cnt;   // per group
+  DBuf<int64_t> g_ids_off, g_blk_off;  // per group, in int32 / double units
+  DBuf<int32_t> lane_ids;             // [nΩ][32] per group
+  DBuf<double> lane_blk;              // [nblk][32] per group
+  std::vector<int64_t> color_goff;    // host, n_colors + 1 (groups are colour-sorted)
 };
+
+constexpr int kLaneMaxSub = 48;
+constexpr int kLaneMaxOmega = 24;
 
 // build_smoother (smoother.hpp:38-58): extract A(Ω,Ω), Cholesky with the
 // jitter retry of factor_spd_block (dense.hpp:175-185), explicit ω columns of

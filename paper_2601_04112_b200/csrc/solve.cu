@@ -127,6 +127,98 @@ void schwarz_launch(const SchwarzView& v, const int32_t* list, int64_t count, co
   LSB_LAUNCH();
 }
 
+// Lane-per-aggregate sweep over groups of 32 same-shape aggregates stored
+// lane-interleaved ([element][lane]): every block load is a 256-byte warp
+// transaction and each lane streams its own block with no cross-lane
+// dependency, so a warp keeps hundreds of independent loads in flight. Per
+// lane the residual patch and the outputs live in a private shared-memory
+// column. MODE 0: RAS overwrite, 1: RAS accumulate, 2: RAS-T accumulate.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_schwarz_lane(SchwarzView v, int64_t g_begin, int64_t g_end,
+                                                      const double* __restrict__ r, double* __restrict__ e, int big,
+                                                      int small) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* wbuf = smem_solve + int64_t(warp) * (big + small) * 32;
+  // RAS reads r[Ω] (big) and forms y[ω] (small); RAS-T the other way round
+  double* R = MODE < 2 ? wbuf : wbuf + int64_t(big) * 32;
+  double* Y = MODE < 2 ? wbuf + int64_t(big) * 32 : wbuf;
+  const int64_t wstride = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t g = g_begin + int64_t(blockIdx.x) * (blockDim.x >> 5) + warp; g < g_end; g += wstride) {
+    const int nw = v.g_nw[g], ng = v.g_ng[g];
+    const int m = nw + ng;
+    const int32_t* ids = v.lane_ids + v.g_ids_off[g];
+    const double* __restrict__ blk = v.lane_blk + v.g_blk_off[g] + lane;
+    const int nin = MODE < 2 ? m : nw;
+    const int nout = MODE < 2 ? nw : m;
+#pragma unroll 8
+    for (int q = 0; q < nin; ++q) {
+      const int id = ids[q * 32 + lane];
+      R[q * 32 + lane] = id >= 0 ? __ldg(&r[id]) : 0.0;
+    }
+    for (int q = 0; q < nout; ++q) Y[q * 32 + lane] = 0.0;
+    int64_t k = 0;
+    for (int i = 0; i < nw; ++i) {  // packed ω×ω upper triangle
+      const double ri = R[i * 32 + lane];
+      double yi = Y[i * 32 + lane];
+#pragma unroll 4
+      for (int j = i; j < nw; ++j) {
+        const double val = __ldcs(&blk[(k + (j - i)) * 32]);
+        yi += val * R[j * 32 + lane];
+        if (j != i) Y[j * 32 + lane] += val * ri;
+      }
+      Y[i * 32 + lane] = yi;
+      k += nw - i;
+    }
+    if (MODE < 2) {
+      for (int i = 0; i < nw; ++i) {  // ω×Γ rows
+        double yi = Y[i * 32 + lane];
+        const double* bi = blk + (k + int64_t(i) * ng) * 32;
+#pragma unroll 8
+        for (int gg = 0; gg < ng; ++gg) yi += __ldcs(&bi[int64_t(gg) * 32]) * R[(nw + gg) * 32 + lane];
+        Y[i * 32 + lane] = yi;
+      }
+      for (int i = 0; i < nw; ++i) {
+        const int id = ids[i * 32 + lane];
+        if (id < 0) continue;
+        if (MODE == 0)
+          e[id] = Y[i * 32 + lane];
+        else
+          e[id] += Y[i * 32 + lane];
+      }
+    } else {
+      for (int i = 0; i < nw; ++i) {  // ω×Γ feeds the Γ outputs
+        const double ri = R[i * 32 + lane];
+        const double* bi = blk + (k + int64_t(i) * ng) * 32;
+#pragma unroll 8
+        for (int gg = 0; gg < ng; ++gg) Y[(nw + gg) * 32 + lane] += __ldcs(&bi[int64_t(gg) * 32]) * ri;
+      }
+      for (int q = 0; q < m; ++q) {
+        const int id = ids[q * 32 + lane];
+        if (id >= 0) e[id] += Y[q * 32 + lane];
+      }
+    }
+  }
+}
+
+template <int MODE>
+void schwarz_lane_launch(const SchwarzView& v, int64_t g_begin, int64_t g_end, const double* r, double* e,
+                         cudaStream_t s) {
+  if (g_end <= g_begin) return;
+  const int big = static_cast<int>(v.max_sub), small = static_cast<int>(v.max_omega);
+  constexpr int WPB = 8;
+  const size_t smem = size_t(WPB) * (big + small) * 32 * 8;
+  static bool attr = false;
+  if (!attr) {
+    LSB_CUDA(cudaFuncSetAttribute(k_schwarz_lane<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    attr = true;
+  }
+  const int64_t per_sm = std::max<int64_t>(1, (220 * 1024) / std::max<size_t>(smem, 1));
+  const int grid = static_cast<int>(std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(g_end - g_begin, WPB), int64_t(sm_count()) * std::min<int64_t>(per_sm, 8))));
+  k_schwarz_lane<MODE><<<grid, WPB * 32, smem, s>>>(v, g_begin, g_end, r, e, big, small);
+  LSB_LAUNCH();
+}
+
 __global__ void k_restrict(InterpView v, const double* __restrict__ res, double* __restrict__ rc) {
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < v.n_coarse; c += int64_t(gridDim.x) * blockDim.x) {
     const int a = v.col_agg[c];
@@ -308,6 +400,13 @@ __global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z,
 }  // namespace
 
 void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumulate, cudaStream_t s) {
+  if (v.n_groups > 0) {
+    if (accumulate)
+      schwarz_lane_launch<1>(v, 0, v.n_groups, r, e, s);
+    else
+      schwarz_lane_launch<0>(v, 0, v.n_groups, r, e, s);
+    return;
+  }
   if (accumulate)
     schwarz_launch<1>(v, nullptr, v.n_agg, r, e, s);
   else
@@ -316,6 +415,11 @@ void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumula
 
 void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, const double* r, double* e,
                   cudaStream_t s) {
+  if (v.n_groups > 0) {
+    const auto& cg = *v.color_goff;
+    for (size_t c = 0; c + 1 < cg.size(); ++c) schwarz_lane_launch<2>(v, cg[c], cg[c + 1], r, e, s);
+    return;
+  }
   for (size_t c = 0; c + 1 < color_off.size(); ++c)
     schwarz_launch<2>(v, v.order + color_off[c], color_off[c + 1] - color_off[c], r, e, s);
 }

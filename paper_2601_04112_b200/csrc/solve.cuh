@@ -17,6 +17,16 @@ struct SchwarzView {
   const double* sm_data;
   const int32_t* order;  // colour-sorted aggregate ids
   int64_t max_omega, max_sub;
+  // lane-interleaved groups (small subdomains), see DevSmoother
+  int64_t n_groups;
+  const int32_t* g_nw;
+  const int32_t* g_ng;
+  const int32_t* g_cnt;
+  const int64_t* g_ids_off;
+  const int64_t* g_blk_off;
+  const int32_t* lane_ids;
+  const double* lane_blk;
+  const std::vector<int64_t>* color_goff;
 };
 
 // RAS (smoother.hpp:65-83, mode RAS): e[ω_i] = (A_i⁻¹ r[Ω_i])|ω  (accumulate

@@ -320,3 +320,15 @@ def test_dense_eigensolver_paths_bit_exact(gpu, oracle_lib, n, path):
     assert st == 0, err.value
     assert np.array_equal(gv, vals)
     assert np.array_equal(gV, vecs)
+
+
+def test_cpp_shim_drop_in(gpu):
+    """The C++ shim (include/lsamgdd_b200/lsamgdd.hpp) used like the reference
+    API by an acceptance.cpp-style caller; built by __graft_entry__.build()."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "shim_demo.bin")
+    if not os.path.exists(exe):
+        pytest.skip("shim_demo.bin not built (needs /root/reference at build time)")
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout + res.stderr
