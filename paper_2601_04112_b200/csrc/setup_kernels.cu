@@ -13,6 +13,7 @@
 #include <tuple>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "dense_dev.cuh"
 #include "setup_kernels.cuh"
@@ -139,6 +140,8 @@ struct GevpArgs {
   int32_t* status;           // per aggregate
   double* gws;
   int64_t ws_stride;
+  const double* pre;         // Grams precomputed by tiled_grams (grams.cu), or null
+  const int64_t* pre_off;    // per aggregate: offset into pre, -1 when not precomputed
 };
 
 __host__ __device__ inline int64_t gevp_ws(int64_t nw, int64_t ng, int64_t maxrow) {
@@ -148,10 +151,25 @@ __host__ __device__ inline int64_t gevp_ws(int64_t nw, int64_t ng, int64_t maxro
   return r2(8) + 2 * r2(nw * nw) + (a > b ? a : b);
 }
 
+// diagnostic hook (LSB_GRAM_CHECK): recompute tiled Grams per team and count mismatches
+__device__ int g_gram_check = 0;
+__device__ unsigned long long g_gram_bad[8];
+// optional per-aggregate phase cycle counters (diagnostic hook, LSB_GEVP_PROF)
+__device__ long long* g_gevp_prof = nullptr;
+
 template <class Team>
 __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* ws, double* fast = nullptr,
                              int64_t fast_cap = 0) {
   const int agg = g.list[idx];
+  long long* const gprof = g_gevp_prof;
+  long long ck = gprof ? clock64() : 0;
+  auto mark = [&](int k) {
+    if (gprof && t.rank() == 0) {
+      const long long now = clock64();
+      gprof[int64_t(agg) * 6 + k] = now - ck;
+      ck = now;
+    }
+  };
   const int32_t* om = g.omega + g.omega_off[agg];
   const int nw = g.omega_off[agg + 1] - g.omega_off[agg];
   const int32_t* ga = g.gamma + g.gamma_off[agg];
@@ -170,10 +188,20 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
   double* B = pa.take(int64_t(ng) * ng);
   int* rpos = pa.take_int(g.maxrow);
   double* rval = pa.take(g.maxrow);
-  t_fill(t, L, 0.0, 2 * r2(int64_t(nw) * nw));
-  t_fill(t, C, 0.0, r2(int64_t(nw) * ng) + r2(int64_t(ng) * ng));
+  const int64_t pre_chk = g.pre_off ? g.pre_off[agg] : -1;
+  const int64_t pre_at = g_gram_check ? -1 : pre_chk;
+  if (pre_at >= 0) {
+    const double* src = g.pre + pre_at;
+    t_copy(t, L, src, int64_t(nw) * nw);
+    t_copy(t, W, src + int64_t(nw) * nw, int64_t(nw) * nw);
+    t_copy(t, C, src + 2 * int64_t(nw) * nw, int64_t(nw) * ng);
+    t_copy(t, B, src + 2 * int64_t(nw) * nw + int64_t(nw) * ng, int64_t(ng) * ng);
+  } else {
+    t_fill(t, L, 0.0, 2 * r2(int64_t(nw) * nw));
+    t_fill(t, C, 0.0, r2(int64_t(nw) * ng) + r2(int64_t(ng) * ng));
+  }
   const bool weighted_lhs = g.p.variant == 1;
-  for (int64_t ri = g.nz_off[agg]; ri < g.nz_off[agg + 1]; ++ri) {
+  for (int64_t ri = pre_at >= 0 ? 0 : g.nz_off[agg]; ri < (pre_at >= 0 ? 0 : g.nz_off[agg + 1]); ++ri) {
     const int r = g.nz[ri];
     const double w = 1.0 / static_cast<double>(g.mult[r]);
     const int64_t k0 = g.goff[r];
@@ -203,6 +231,30 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
     }
     t.sync();
   }
+  if (g_gram_check && pre_chk >= 0) {  // diagnostic: compare the tiled Grams with this sweep
+    const double* src = g.pre + pre_chk;
+    const double* mats[4] = {L, W, C, B};
+    const int64_t sz[4] = {int64_t(nw) * nw, int64_t(nw) * nw, int64_t(nw) * ng, int64_t(ng) * ng};
+    int64_t at = 0;
+    for (int q = 0; q < 4; ++q) {
+      for (int64_t e = t.rank(); e < sz[q]; e += t.size()) {
+        const double a = mats[q][e], b = src[at + e];
+        if (__double_as_longlong(a) != __double_as_longlong(b)) {
+          const unsigned long long k = atomicAdd(&g_gram_bad[0], 1ull);
+          if (k == 0) {
+            g_gram_bad[1] = agg;
+            g_gram_bad[2] = q;
+            g_gram_bad[3] = e;
+            g_gram_bad[4] = __double_as_longlong(a);
+            g_gram_bad[5] = __double_as_longlong(b);
+          }
+        }
+      }
+      at += sz[q];
+    }
+    t.sync();
+  }
+  mark(0);
   if (ng > 0) {
     double* Pm = pa.take(int64_t(ng) * ng);
     double* T = pa.take(int64_t(ng) * nw);
@@ -212,6 +264,7 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
       if (t.rank() == 0) g.status[agg] = st;
       return;
     }
+    mark(1);
     // T = pinv·crossᵀ, S = cross·T (dense.hpp:47-59 with the transposed copy)
     for (int64_t e = t.rank(); e < int64_t(ng) * nw; e += t.size()) {
       const int i = static_cast<int>(e / nw), j = static_cast<int>(e % nw);
@@ -229,6 +282,7 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
     t.sync();
   }
   t_symmetrize(t, W, nw);
+  mark(2);
 
   // ---- phase B: pencil, keep rule, MGS, sign rule
   Arena pb = base;
@@ -242,6 +296,7 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
     if (t.rank() == 0) g.status[agg] = st;
     return;
   }
+  mark(3);
   for (int k = t.rank(); k < cnt; k += t.size()) g.spec[g.spec_off[agg] + k] = values[k];
   if (t.rank() == 0) g.nspec[agg] = cnt;
   for (int k = 0; k < cnt; ++k)
@@ -307,6 +362,7 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
     if (t.rank() == 0) g.kcols[agg] = cols;
   }
   t.sync();
+  mark(4);
 }
 
 extern __shared__ double dyn_smem[];
@@ -854,6 +910,41 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
   DBuf<int32_t> kcols(na, s), nspec(na, s), status(na, s);
   status.zero(s);
   nspec.zero(s);
+  {
+    const int chk = getenv("LSB_GRAM_CHECK") ? 1 : 0;
+    unsigned long long z[8] = {0};
+    LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_check, &chk, sizeof(chk), 0, cudaMemcpyHostToDevice, s));
+    LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_bad, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+  }
+  const bool prof_on = getenv("LSB_GEVP_PROF") != nullptr;
+  DBuf<long long> gprof(prof_on ? na * 6 : 1, s);
+  if (prof_on) {
+    gprof.zero(s);
+    long long* gp_ptr = gprof.get();
+    LSB_CUDA(cudaMemcpyToSymbol(g_gevp_prof, &gp_ptr, sizeof(gp_ptr)));
+  }
+  // Grams of large subdomains: multi-CTA tiles (grams.cu) instead of one team
+  DBuf<double> pre;
+  DBuf<int64_t> pre_off;
+  {
+    std::vector<int32_t> big;
+    std::vector<int64_t> hpo(na, -1);
+    int64_t tot = 0;
+    for (int64_t i = 0; i < na; ++i) {
+      const int64_t nw = hoo[i + 1] - hoo[i], ng = hgo[i + 1] - hgo[i];
+      if (nw + ng >= kTileMinSub && nw + ng <= kTileMaxSub) {
+        big.push_back(static_cast<int32_t>(i));
+        hpo[i] = tot;
+        tot += pre_gram_doubles(nw, ng);
+      }
+    }
+    if (!big.empty()) {
+      const auto h_nzo = rs.nz_off.download(s);
+      pre.alloc(tot, s);
+      pre_off.upload(hpo, s);
+      tiled_grams(gm, topo, hoo, hgo, rs, h_nzo, big, gp.variant == 1 ? 1 : 0, pre.get(), pre_off.get(), s);
+    }
+  }
   // chunk aggregates (id order) so the nω² panel scratch stays bounded
   const int64_t budget = int64_t(1) << 27;  // doubles (1 GiB)
   std::vector<int32_t> h_k(na, 0);
@@ -921,9 +1012,35 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     g.kcols = kcols.get();
     g.nspec = nspec.get();
     g.status = status.get();
+    g.pre = pre.get();
+    g.pre_off = pre.get() ? pre_off.get() : nullptr;
     std::vector<int32_t> lo;
     launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, s);
     chunk_list[ci].upload(lo, s);
+  }
+  if (prof_on) {
+    const auto hp = gprof.download(s);
+    long long mx[6] = {0}, sm[6] = {0};
+    for (int64_t i = 0; i < na; ++i)
+      for (int k = 0; k < 5; ++k) {
+        mx[k] = std::max(mx[k], hp[i * 6 + k]);
+        sm[k] += hp[i * 6 + k];
+      }
+    fprintf(stderr, "gevp prof level %d (%lld aggs) Mcycles max/sum: grams %.1f/%.1f pinv %.1f/%.1f schur %.1f/%.1f "
+            "spsd_gevp %.1f/%.1f mgs %.1f/%.1f\n", gp.level, (long long)na, mx[0] / 1e6, sm[0] / 1e6, mx[1] / 1e6,
+            sm[1] / 1e6, mx[2] / 1e6, sm[2] / 1e6, mx[3] / 1e6, sm[3] / 1e6, mx[4] / 1e6, sm[4] / 1e6);
+    long long* np = nullptr;
+    LSB_CUDA(cudaMemcpyToSymbol(g_gevp_prof, &np, sizeof(np)));
+  }
+  if (getenv("LSB_GRAM_CHECK") && pre.get()) {
+    unsigned long long hb[8];
+    LSB_CUDA(cudaMemcpyFromSymbolAsync(hb, g_gram_bad, sizeof(hb), 0, cudaMemcpyDeviceToHost, s));
+    LSB_CUDA(cudaStreamSynchronize(s));
+    double va, vb;
+    memcpy(&va, &hb[4], 8);
+    memcpy(&vb, &hb[5], 8);
+    fprintf(stderr, "gram check level %d: %llu mismatches; first agg %llu mat %llu idx %llu team %.17g tiled %.17g\n",
+            gp.level, hb[0], hb[1], hb[2], hb[3], va, vb);
   }
   const auto hs = status.download(s);
   for (int64_t i = 0; i < na; ++i) {

@@ -84,6 +84,17 @@ void local_gevp_all(const DevCsr& g, const DevTopo& topo, const std::vector<int3
                     const std::vector<int32_t>& h_gamma_off, const DevRowSets& rs, const std::vector<int64_t>& h_nz_off,
                     const GevpParams& gp, DevInterp& ip, DevCsr& p, bool keep_spectra, cudaStream_t s);
 
+// Local Grams of large subdomains as multi-CTA tiles (grams.cu): for each
+// listed aggregate, L (nω²), W (nω²), C (nω×nΓ), B (nΓ²) row-major at
+// out + out_off[agg], bit-identical to the per-aggregate sweep.
+constexpr int64_t kTileMinSub = 96;
+constexpr int64_t kTileMaxSub = 4096;
+int64_t pre_gram_doubles(int64_t nw, int64_t ng);
+void tiled_grams(const DevCsr& gm, const DevTopo& topo, const std::vector<int32_t>& hoo,
+                 const std::vector<int32_t>& hgo, const DevRowSets& rs, const std::vector<int64_t>& h_nz_off,
+                 const std::vector<int32_t>& aggs, int weighted_lhs, double* out, const int64_t* d_out_off,
+                 cudaStream_t s);
+
 // One dense eigensolve through a chosen device path (0 warp team, 1 CTA
 // team, 2 CTA pipelined); returns 0 or the EigError code. Test hook.
 int dense_sym_eig(int64_t n, const double* a, double* vals, double* vecs, int path, cudaStream_t s);
