@@ -307,6 +307,15 @@ SchwarzView Level::schwarz_view() const {
   v.lane_ids = sm.lane_ids.get();
   v.lane_blk = sm.lane_blk.get();
   v.color_goff = &sm.color_goff;
+  v.rows = sm.rows;
+  v.row_off = sm.row_off.get();
+  v.row_data = sm.row_data.get();
+  v.ras_agg = sm.ras_agg.get();
+  v.ras_row = sm.ras_row.get();
+  v.n_ras_items = static_cast<int64_t>(sm.ras_agg.size());
+  v.rast_agg = sm.rast_agg.get();
+  v.rast_row = sm.rast_row.get();
+  v.rast_color_off = &sm.rast_color_off;
   return v;
 }
 

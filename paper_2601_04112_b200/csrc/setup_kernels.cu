@@ -608,6 +608,72 @@ void build_lane_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, con
   LSB_LAUNCH();
 }
 
+// ---- row layout of large Schwarz blocks -------------------------------------------
+
+__global__ void k_expand_rows(const int32_t* omega_off, const int32_t* gamma_off, const int64_t* sm_off,
+                              const double* sm_data, const int64_t* row_off, double* row_data, int64_t n_agg) {
+  for (int64_t a = blockIdx.x; a < n_agg; a += gridDim.x) {
+    const int nw = omega_off[a + 1] - omega_off[a], ng = gamma_off[a + 1] - gamma_off[a];
+    const int m = nw + ng;
+    const double* pk = sm_data + sm_off[a];
+    const double* pg = pk + int64_t(nw) * (nw + 1) / 2;
+    double* F = row_data + row_off[a];
+    double* Gt = F + int64_t(nw) * m;
+    for (int64_t e = threadIdx.x; e < int64_t(nw) * m; e += blockDim.x) {
+      const int i = static_cast<int>(e / m), j = static_cast<int>(e % m);
+      double v;
+      if (j < nw) {
+        const int lo = i < j ? i : j, hi = i < j ? j : i;
+        v = pk[int64_t(lo) * nw - (int64_t(lo) * (lo - 1)) / 2 + (hi - lo)];
+      } else {
+        v = pg[int64_t(i) * ng + (j - nw)];
+      }
+      F[e] = v;
+    }
+    for (int64_t e = threadIdx.x; e < int64_t(ng) * nw; e += blockDim.x) {
+      const int g = static_cast<int>(e / nw), i = static_cast<int>(e % nw);
+      Gt[e] = pg[int64_t(i) * ng + g];
+    }
+  }
+}
+
+void build_row_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, const std::vector<int32_t>& hgo,
+                      const std::vector<int32_t>& byc, DevSmoother& sm, cudaStream_t s) {
+  const int64_t na = topo.n_agg;
+  std::vector<int64_t> roff(na + 1, 0);
+  std::vector<int32_t> ra, rr, ta, tr;
+  for (int64_t i = 0; i < na; ++i) {
+    const int64_t nw = hoo[i + 1] - hoo[i], ng = hgo[i + 1] - hgo[i];
+    roff[i + 1] = roff[i] + nw * (nw + ng) + ng * nw;
+    for (int64_t r = 0; r < nw; ++r) {
+      ra.push_back(static_cast<int32_t>(i));
+      rr.push_back(static_cast<int32_t>(r));
+    }
+  }
+  sm.rast_color_off.assign(sm.color_off.size(), 0);
+  for (size_t c = 0; c + 1 < sm.color_off.size(); ++c) {
+    for (int64_t k = sm.color_off[c]; k < sm.color_off[c + 1]; ++k) {
+      const int32_t a = byc[k];
+      const int64_t m = (hoo[a + 1] - hoo[a]) + (hgo[a + 1] - hgo[a]);
+      for (int64_t r = 0; r < m; ++r) {
+        ta.push_back(a);
+        tr.push_back(static_cast<int32_t>(r));
+      }
+    }
+    sm.rast_color_off[c + 1] = static_cast<int64_t>(ta.size());
+  }
+  sm.row_off.upload(roff, s);
+  sm.row_data.alloc(std::max<int64_t>(roff[na], 1), s);
+  sm.ras_agg.upload(ra, s);
+  sm.ras_row.upload(rr, s);
+  sm.rast_agg.upload(ta, s);
+  sm.rast_row.upload(tr, s);
+  k_expand_rows<<<static_cast<int>(std::min<int64_t>(std::max<int64_t>(na, 1), sm_count() * 8)), 256, 0, s>>>(
+      topo.omega_off.get(), topo.gamma_off.get(), sm.off.get(), sm.data.get(), sm.row_off.get(), sm.row_data.get(),
+      na);
+  LSB_LAUNCH();
+}
+
 // ---- coarse factor -------------------------------------------------------------
 
 __global__ void k_coarse_dense(const int64_t* off, const int32_t* col, const double* val, int64_t n, double* d) {
@@ -837,6 +903,11 @@ void row_sets(const DevCsr& g, const DevTopo& topo, DevRowSets& rs, cudaStream_t
   rs.max_row_nnz = static_cast<int64_t>(h[2]);
 }
 
+namespace {
+void build_row_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, const std::vector<int32_t>& hgo,
+                      const std::vector<int32_t>& byc, DevSmoother& sm, cudaStream_t s);
+}
+
 void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int32_t>& hoo,
                     const std::vector<int32_t>& hgo, const std::vector<int64_t>& colors, int64_t n_colors,
                     DevSmoother& sm, cudaStream_t s) {
@@ -890,6 +961,9 @@ void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int3
   std::vector<int64_t> cur(sm.color_off.begin(), sm.color_off.end() - 1);
   for (int64_t i = 0; i < na; ++i) byc[cur[colors[i]]++] = static_cast<int32_t>(i);
   sm.order.upload(byc, s);
+  const int64_t max_blk = sm.max_omega * (sm.max_omega + 1) / 2 + sm.max_omega * (sm.max_sub - sm.max_omega);
+  sm.rows = sm.n_groups == 0 && (max_blk > kRowsMinBlk || sm.max_sub > 512);
+  if (sm.rows) build_row_layout(topo, hoo, hgo, byc, sm, s);
 }
 
 void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int32_t>& hoo,

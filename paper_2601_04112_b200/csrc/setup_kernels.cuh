@@ -47,9 +47,20 @@ struct DevSmoother {
   DBuf<int32_t> lane_ids;             // [nΩ][32] per group
   DBuf<double> lane_blk;              // [nblk][32] per group
   std::vector<int64_t> color_goff;    // host, n_colors + 1 (groups are colour-sorted)
+  // Row layout for large subdomains (warp per output row, many warps per
+  // aggregate): per aggregate the full ω×Ω rows of the inverse (F, nω×nΩ)
+  // then its Γ columns transposed (Gt, nΓ×nω), so that RAS (rows of F) and
+  // RAS-T (ω rows of F, rows of Gt) read contiguous rows.
+  bool rows = false;
+  DBuf<int64_t> row_off;              // n_agg + 1 (doubles)
+  DBuf<double> row_data;
+  DBuf<int32_t> ras_agg, ras_row;     // RAS work items: (aggregate, ω row)
+  DBuf<int32_t> rast_agg, rast_row;   // RAS-T work items, colour-sorted: (aggregate, Ω row)
+  std::vector<int64_t> rast_color_off;  // host, n_colors + 1
 };
 
 constexpr int kLaneMaxSub = 48;
+constexpr int64_t kRowsMinBlk = 2048;  // larger blocks use the row layout (warp per output row)
 constexpr int kLaneMaxOmega = 24;
 
 // build_smoother (smoother.hpp:38-58): extract A(Ω,Ω), Cholesky with the

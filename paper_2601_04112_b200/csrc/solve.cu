@@ -219,6 +219,70 @@ void schwarz_lane_launch(const SchwarzView& v, int64_t g_begin, int64_t g_end, c
   LSB_LAUNCH();
 }
 
+// Row layout (large subdomains): one warp per output row, lanes over a
+// contiguous row of the explicit inverse, fixed xor-tree reduction (the
+// result is deterministic). RAS (MODE 0/1): row i of F · r[Ω] -> e[ω_i];
+// RAS-T (MODE 2): row j of [F_ωω; Gt] · r[ω] -> e[Ω_j] += (one colour per
+// launch: disjoint Ω, no atomics).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_schwarz_rows(SchwarzView v, const int32_t* __restrict__ item_agg,
+                                                      const int32_t* __restrict__ item_row, int64_t i0, int64_t i1,
+                                                      const double* __restrict__ r, double* __restrict__ e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t it = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < i1; it += warps) {
+    const int a = item_agg[it], row = item_row[it];
+    const int32_t* om = v.omega + v.omega_off[a];
+    const int nw = v.omega_off[a + 1] - v.omega_off[a];
+    const int32_t* ga = v.gamma + v.gamma_off[a];
+    const int ng = v.gamma_off[a + 1] - v.gamma_off[a];
+    const int m = nw + ng;
+    const double* F = v.row_data + v.row_off[a];
+    double s0 = 0.0, s1 = 0.0;
+    if (MODE < 2) {
+      const double* fr = F + int64_t(row) * m;
+      int j = lane;
+      for (; j + 32 < m; j += 64) {
+        const int c0 = j < nw ? om[j] : ga[j - nw];
+        const int c1 = j + 32 < nw ? om[j + 32] : ga[j + 32 - nw];
+        s0 += __ldcs(&fr[j]) * __ldg(&r[c0]);
+        s1 += __ldcs(&fr[j + 32]) * __ldg(&r[c1]);
+      }
+      if (j < m) s0 += __ldcs(&fr[j]) * __ldg(&r[j < nw ? om[j] : ga[j - nw]]);
+    } else {
+      const double* fr = row < nw ? F + int64_t(row) * m : F + int64_t(nw) * m + int64_t(row - nw) * nw;
+      int i = lane;
+      for (; i + 32 < nw; i += 64) {
+        s0 += __ldcs(&fr[i]) * __ldg(&r[om[i]]);
+        s1 += __ldcs(&fr[i + 32]) * __ldg(&r[om[i + 32]]);
+      }
+      if (i < nw) s0 += __ldcs(&fr[i]) * __ldg(&r[om[i]]);
+    }
+    double sum = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) {
+      if (MODE == 0) {
+        e[om[row]] = sum;
+      } else if (MODE == 1) {
+        e[om[row]] += sum;
+      } else {
+        const int c = row < nw ? om[row] : ga[row - nw];
+        e[c] += sum;
+      }
+    }
+  }
+}
+
+template <int MODE>
+void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t* ir, int64_t i0, int64_t i1,
+                         const double* r, double* e, cudaStream_t s) {
+  if (i1 <= i0) return;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * 8)));
+  k_schwarz_rows<MODE><<<grid, 256, 0, s>>>(v, ia, ir, i0, i1, r, e);
+  LSB_LAUNCH();
+}
+
 __global__ void k_restrict(InterpView v, const double* __restrict__ res, double* __restrict__ rc) {
   for (int64_t c = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; c < v.n_coarse; c += int64_t(gridDim.x) * blockDim.x) {
     const int a = v.col_agg[c];
@@ -400,6 +464,13 @@ __global__ void k_update_p(double* __restrict__ p, const double* __restrict__ z,
 }  // namespace
 
 void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumulate, cudaStream_t s) {
+  if (v.rows) {
+    if (accumulate)
+      schwarz_rows_launch<1>(v, v.ras_agg, v.ras_row, 0, v.n_ras_items, r, e, s);
+    else
+      schwarz_rows_launch<0>(v, v.ras_agg, v.ras_row, 0, v.n_ras_items, r, e, s);
+    return;
+  }
   if (v.n_groups > 0) {
     if (accumulate)
       schwarz_lane_launch<1>(v, 0, v.n_groups, r, e, s);
@@ -415,6 +486,11 @@ void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumula
 
 void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, const double* r, double* e,
                   cudaStream_t s) {
+  if (v.rows) {
+    const auto& co = *v.rast_color_off;
+    for (size_t c = 0; c + 1 < co.size(); ++c) schwarz_rows_launch<2>(v, v.rast_agg, v.rast_row, co[c], co[c + 1], r, e, s);
+    return;
+  }
   if (v.n_groups > 0) {
     const auto& cg = *v.color_goff;
     for (size_t c = 0; c + 1 < cg.size(); ++c) schwarz_lane_launch<2>(v, cg[c], cg[c + 1], r, e, s);

@@ -27,6 +27,16 @@ struct SchwarzView {
   const int32_t* lane_ids;
   const double* lane_blk;
   const std::vector<int64_t>* color_goff;
+  // row layout (large subdomains), see DevSmoother
+  bool rows;
+  const int64_t* row_off;
+  const double* row_data;
+  const int32_t* ras_agg;
+  const int32_t* ras_row;
+  int64_t n_ras_items;
+  const int32_t* rast_agg;
+  const int32_t* rast_row;
+  const std::vector<int64_t>* rast_color_off;
 };
 
 // RAS (smoother.hpp:65-83, mode RAS): e[ω_i] = (A_i⁻¹ r[Ω_i])|ω  (accumulate
