@@ -307,6 +307,10 @@ SchwarzView Level::schwarz_view() const {
   v.lane_ids = sm.lane_ids.get();
   v.lane_blk = sm.lane_blk.get();
   v.color_goff = &sm.color_goff;
+  v.lane_ras_items = sm.lane_ras_items.get();
+  v.n_lane_ras_items = static_cast<int64_t>(sm.lane_ras_items.size());
+  v.lane_rast_items = sm.lane_rast_items.get();
+  v.lane_rast_color_off = &sm.lane_rast_color_off;
   v.rows = sm.rows;
   v.row_off = sm.row_off.get();
   v.row_data = sm.row_data.get();
@@ -491,6 +495,14 @@ SolveWs::~SolveWs() {
   }
 }
 
+// res = r - A_l e: SELL thread-per-row on short rows, warp per row on long ones
+static void level_residual(const Level& L, const double* e, double* res, const double* r, cudaStream_t s) {
+  if (L.A.nr > 0 && L.A.nnz >= 48 * L.A.nr)
+    csr_spmv_warp(L.A, e, res, r, s);
+  else
+    sell_spmv(L.A_sell, e, res, r, s);
+}
+
 void vcycle(const Hierarchy& h, SolveWs& ws, int64_t level, const double* r, double* e) {
   if (level < 0 || level >= static_cast<int64_t>(h.levels.size())) raise(LSAMGDD_ERR_INDEX, "vcycle: level out of range");
   const Level& L = h.levels[level];
@@ -509,11 +521,11 @@ void vcycle(const Hierarchy& h, SolveWs& ws, int64_t level, const double* r, dou
       schwarz_ras(sv, r, e, false, s);  // e = 0 + RAS(r - A·0)
       if (ws.timing && level == 0) LSB_CUDA(cudaEventRecordWithFlags(ws.ev[1], s, cudaEventRecordExternal));
     } else {
-      sell_spmv(L.A_sell, e, res, r, s);
+      level_residual(L, e, res, r, s);
       schwarz_ras(sv, res, e, true, s);
     }
   }
-  sell_spmv(L.A_sell, e, res, r, s);
+  level_residual(L, e, res, r, s);
   double* rc = ws.rhs[level + 1].get();
   double* ec = ws.e[level + 1].get();
   const InterpView iv = L.interp_view();
@@ -521,7 +533,7 @@ void vcycle(const Hierarchy& h, SolveWs& ws, int64_t level, const double* r, dou
   vcycle(h, ws, level + 1, rc, ec);
   prolong_add(iv, ec, e, s);
   for (uint64_t sw = 0; sw < h.params.post_sweeps; ++sw) {
-    sell_spmv(L.A_sell, e, res, r, s);
+    level_residual(L, e, res, r, s);
     const bool tm = ws.timing && level == 0 && sw == 0;
     if (tm) LSB_CUDA(cudaEventRecordWithFlags(ws.ev[2], s, cudaEventRecordExternal));
     schwarz_rast(sv, L.sm.color_off, res, e, s);

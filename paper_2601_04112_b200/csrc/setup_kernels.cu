@@ -592,6 +592,19 @@ void build_lane_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, con
   }
   for (int64_t c = 0; c < n_colors; ++c) sm.color_goff[c + 1] += sm.color_goff[c];
   sm.n_groups = static_cast<int64_t>(g_nw.size());
+  {
+    std::vector<int32_t> ri, ti;
+    sm.lane_rast_color_off.assign(n_colors + 1, 0);
+    for (int64_t g = 0; g < sm.n_groups; ++g)
+      for (int r = 0; r < g_nw[g]; ++r) ri.push_back(static_cast<int32_t>((g << 8) | r));
+    for (int64_t c = 0; c < n_colors; ++c) {
+      for (int64_t g = sm.color_goff[c]; g < sm.color_goff[c + 1]; ++g)
+        for (int r = 0; r < g_nw[g] + g_ng[g]; ++r) ti.push_back(static_cast<int32_t>((g << 8) | r));
+      sm.lane_rast_color_off[c + 1] = static_cast<int64_t>(ti.size());
+    }
+    sm.lane_ras_items.upload(ri, s);
+    sm.lane_rast_items.upload(ti, s);
+  }
   DBuf<int32_t> d_agg;
   d_agg.upload(g_agg, s);
   sm.g_nw.upload(g_nw, s);

@@ -47,6 +47,9 @@ struct DevSmoother {
   DBuf<int32_t> lane_ids;             // [nΩ][32] per group
   DBuf<double> lane_blk;              // [nblk][32] per group
   std::vector<int64_t> color_goff;    // host, n_colors + 1 (groups are colour-sorted)
+  // warp-per-output-row work items over the groups: (group << 8) | row
+  DBuf<int32_t> lane_ras_items, lane_rast_items;
+  std::vector<int64_t> lane_rast_color_off;  // host, n_colors + 1
   // Row layout for large subdomains (warp per output row, many warps per
   // aggregate): per aggregate the full ω×Ω rows of the inverse (F, nω×nΩ)
   // then its Γ columns transposed (Gt, nΓ×nω), so that RAS (rows of F) and
@@ -60,7 +63,7 @@ struct DevSmoother {
 };
 
 constexpr int kLaneMaxSub = 48;
-constexpr int64_t kRowsMinBlk = 2048;  // larger blocks use the row layout (warp per output row)
+constexpr int64_t kRowsMinBlk = 0;  // larger blocks use the row layout (warp per output row)
 constexpr int kLaneMaxOmega = 24;
 
 // build_smoother (smoother.hpp:38-58): extract A(Ω,Ω), Cholesky with the

@@ -219,6 +219,91 @@ void schwarz_lane_launch(const SchwarzView& v, int64_t g_begin, int64_t g_end, c
   LSB_LAUNCH();
 }
 
+// Lane-interleaved groups, one warp per (group, output row): lane l computes
+// row `row` of aggregate l of the group, so every block load is one 256-byte
+// warp transaction and each lane has nΩ (RAS) or nω (RAS-T) independent
+// loads in flight. The ω×ω triangle is read by both of its rows (L1 keeps
+// the second read on chip: the rows of a group are consecutive items).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_schwarz_lrow(SchwarzView v, const int32_t* __restrict__ items, int64_t i0,
+                                                      int64_t i1, const double* __restrict__ r,
+                                                      double* __restrict__ e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t it = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < i1; it += warps) {
+    const int code = items[it];
+    const int g = code >> 8, row = code & 255;
+    const int nw = v.g_nw[g], ng = v.g_ng[g];
+    const int32_t* ids = v.lane_ids + v.g_ids_off[g] + lane;
+    const double* __restrict__ blk = v.lane_blk + v.g_blk_off[g] + lane;
+    const int64_t p0 = int64_t(nw) * (nw + 1) / 2;
+    const int out = ids[row * 32];
+    double s0 = 0.0, s1 = 0.0;
+    if (MODE < 2) {
+#pragma unroll 4
+      for (int j = 0; j < nw; ++j) {
+        const int lo = row < j ? row : j, hi = row < j ? j : row;
+        const int64_t k = int64_t(lo) * nw - (int64_t(lo) * (lo - 1)) / 2 + (hi - lo);
+        const int id = ids[j * 32];
+        const double rv = id >= 0 ? __ldg(&r[id]) : 0.0;
+        if (j & 1)
+          s1 += __ldg(&blk[k * 32]) * rv;
+        else
+          s0 += __ldg(&blk[k * 32]) * rv;
+      }
+      const double* bg = blk + (p0 + int64_t(row) * ng) * 32;
+#pragma unroll 8
+      for (int q = 0; q < ng; ++q) {
+        const int id = ids[(nw + q) * 32];
+        const double rv = id >= 0 ? __ldg(&r[id]) : 0.0;
+        if (q & 1)
+          s1 += __ldcs(&bg[int64_t(q) * 32]) * rv;
+        else
+          s0 += __ldcs(&bg[int64_t(q) * 32]) * rv;
+      }
+    } else if (row < nw) {
+#pragma unroll 4
+      for (int i = 0; i < nw; ++i) {
+        const int lo = row < i ? row : i, hi = row < i ? i : row;
+        const int64_t k = int64_t(lo) * nw - (int64_t(lo) * (lo - 1)) / 2 + (hi - lo);
+        const int id = ids[i * 32];
+        const double rv = id >= 0 ? __ldg(&r[id]) : 0.0;
+        if (i & 1)
+          s1 += __ldg(&blk[k * 32]) * rv;
+        else
+          s0 += __ldg(&blk[k * 32]) * rv;
+      }
+    } else {
+      const double* bg = blk + (p0 + (row - nw)) * 32;
+#pragma unroll 4
+      for (int i = 0; i < nw; ++i) {
+        const int id = ids[i * 32];
+        const double rv = id >= 0 ? __ldg(&r[id]) : 0.0;
+        if (i & 1)
+          s1 += __ldcs(&bg[int64_t(i) * ng * 32]) * rv;
+        else
+          s0 += __ldcs(&bg[int64_t(i) * ng * 32]) * rv;
+      }
+    }
+    if (out >= 0) {
+      const double sum = s0 + s1;
+      if (MODE == 0)
+        e[out] = sum;
+      else
+        e[out] += sum;
+    }
+  }
+}
+
+template <int MODE>
+void schwarz_lrow_launch(const SchwarzView& v, const int32_t* items, int64_t i0, int64_t i1, const double* r, double* e,
+                         cudaStream_t s) {
+  if (i1 <= i0) return;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * 16)));
+  k_schwarz_lrow<MODE><<<grid, 256, 0, s>>>(v, items, i0, i1, r, e);
+  LSB_LAUNCH();
+}
+
 // Row layout (large subdomains): one warp per output row, lanes over a
 // contiguous row of the explicit inverse, fixed xor-tree reduction (the
 // result is deterministic). RAS (MODE 0/1): row i of F · r[Ω] -> e[ω_i];
@@ -298,6 +383,27 @@ __global__ void k_restrict(InterpView v, const double* __restrict__ res, double*
       s += pan[int64_t(rr) * k + j] * x;
     }
     rc[c] = s;
+  }
+}
+
+// Pᵀ res with one warp per coarse column (large aggregates): lanes over the
+// aggregate's fine rows, fixed xor-tree reduction.
+__global__ void __launch_bounds__(256) k_restrict_warp(InterpView v, const double* __restrict__ res,
+                                                       double* __restrict__ rc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t c = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); c < v.n_coarse; c += warps) {
+    const int a = v.col_agg[c];
+    const int j = static_cast<int>(c - v.coarse_off[a]);
+    const int k = v.coarse_off[a + 1] - v.coarse_off[a];
+    const double* pan = v.panels + v.panel_off[a];
+    const int32_t* om = v.omega + v.omega_off[a];
+    const int nw = v.omega_off[a + 1] - v.omega_off[a];
+    double s = 0.0;
+    for (int rr = lane; rr < nw; rr += 32) s += pan[int64_t(rr) * k + j] * res[om[rr]];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) rc[c] = s;
   }
 }
 
@@ -473,9 +579,9 @@ void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumula
   }
   if (v.n_groups > 0) {
     if (accumulate)
-      schwarz_lane_launch<1>(v, 0, v.n_groups, r, e, s);
+      schwarz_lrow_launch<1>(v, v.lane_ras_items, 0, v.n_lane_ras_items, r, e, s);
     else
-      schwarz_lane_launch<0>(v, 0, v.n_groups, r, e, s);
+      schwarz_lrow_launch<0>(v, v.lane_ras_items, 0, v.n_lane_ras_items, r, e, s);
     return;
   }
   if (accumulate)
@@ -492,8 +598,8 @@ void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, c
     return;
   }
   if (v.n_groups > 0) {
-    const auto& cg = *v.color_goff;
-    for (size_t c = 0; c + 1 < cg.size(); ++c) schwarz_lane_launch<2>(v, cg[c], cg[c + 1], r, e, s);
+    const auto& co = *v.lane_rast_color_off;
+    for (size_t c = 0; c + 1 < co.size(); ++c) schwarz_lrow_launch<2>(v, v.lane_rast_items, co[c], co[c + 1], r, e, s);
     return;
   }
   for (size_t c = 0; c + 1 < color_off.size(); ++c)
@@ -502,7 +608,12 @@ void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, c
 
 void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s) {
   if (v.n_coarse == 0) return;
-  k_restrict<<<grid_for(v.n_coarse), 256, 0, s>>>(v, res, rc);
+  if (v.n_coarse > 0 && v.n_fine >= 64 * v.n_agg) {  // large aggregates: warp per coarse column
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(v.n_coarse, 8), int64_t(sm_count()) * 16)));
+    k_restrict_warp<<<grid, 256, 0, s>>>(v, res, rc);
+  } else {
+    k_restrict<<<grid_for(v.n_coarse), 256, 0, s>>>(v, res, rc);
+  }
   LSB_LAUNCH();
 }
 

@@ -27,6 +27,10 @@ struct SchwarzView {
   const int32_t* lane_ids;
   const double* lane_blk;
   const std::vector<int64_t>* color_goff;
+  const int32_t* lane_ras_items;
+  int64_t n_lane_ras_items;
+  const int32_t* lane_rast_items;
+  const std::vector<int64_t>* lane_rast_color_off;
   // row layout (large subdomains), see DevSmoother
   bool rows;
   const int64_t* row_off;

@@ -207,7 +207,42 @@ __global__ void __launch_bounds__(256) k_sell_spmv(const int64_t* __restrict__ s
   }
 }
 
+// CSR, one warp per row (long rows of the coarse levels): lanes stride the
+// row with two accumulators, fixed xor-tree reduction (deterministic).
+template <int MODE>
+__global__ void __launch_bounds__(256) k_csr_spmv_warp(const int64_t* __restrict__ off, const int32_t* __restrict__ col,
+                                                       const double* __restrict__ val, int64_t nr,
+                                                       const double* __restrict__ x, double* __restrict__ y,
+                                                       const double* __restrict__ r) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < nr; i += warps) {
+    const int64_t b = off[i], e = off[i + 1];
+    double s0 = 0.0, s1 = 0.0;
+    int64_t k = b + lane;
+    for (; k + 32 < e; k += 64) {
+      s0 += __ldcs(&val[k]) * __ldg(&x[__ldcs(&col[k])]);
+      s1 += __ldcs(&val[k + 32]) * __ldg(&x[__ldcs(&col[k + 32])]);
+    }
+    if (k < e) s0 += __ldcs(&val[k]) * __ldg(&x[__ldcs(&col[k])]);
+    double sum = s0 + s1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (lane == 0) y[i] = MODE == 0 ? sum : r[i] - sum;
+  }
+}
+
 }  // namespace
+
+void csr_spmv_warp(const DevCsr& a, const double* x, double* y, const double* r, cudaStream_t s) {
+  if (a.nr == 0) return;
+  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(a.nr, 8), int64_t(sm_count()) * 16)));
+  if (r)
+    k_csr_spmv_warp<1><<<grid, 256, 0, s>>>(a.off.get(), a.col.get(), a.val.get(), a.nr, x, y, r);
+  else
+    k_csr_spmv_warp<0><<<grid, 256, 0, s>>>(a.off.get(), a.col.get(), a.val.get(), a.nr, x, y, r);
+  LSB_LAUNCH();
+}
 
 int sm_count() {
   static int n = [] {

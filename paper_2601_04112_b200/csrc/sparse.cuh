@@ -46,5 +46,7 @@ void sell_from_csr(const DevCsr& a, Sell& out, cudaStream_t s);
 // y = A x (mode 0), y = r - A x (mode 1, the fused V-cycle residual of
 // hierarchy.hpp:213-214). Thread per row, sequential in CSR order.
 void sell_spmv(const Sell& a, const double* x, double* y, const double* r, cudaStream_t s);
+// y = A x (r == null) or y = r - A x with one warp per row (long rows)
+void csr_spmv_warp(const DevCsr& a, const double* x, double* y, const double* r, cudaStream_t s);
 
 }  // namespace lsb
