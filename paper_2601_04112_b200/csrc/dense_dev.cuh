@@ -653,6 +653,8 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
   return 0;
 }
 
+#include "jacobi2.cuh"
+
 __device__ int g_eig_split = 1;
   // 1: producer/consumer, 0: one barrier per rotation (test hook)
 
@@ -754,6 +756,21 @@ __device__ int t_sym_eig(const Team& t, int n, const double* m, double* vals, do
     return 0;
   }
   if constexpr (!std::is_same<Team, WarpTeam>::value) {
+    if (ar.fast && n >= 48 && blockDim.x == kPipeThreads && g_eig_split == 2 && n <= 768) {
+      int RA = 12, NO = 22;
+      while (jac2_smem_doubles(n, RA, NO) > ar.fast_cap && RA > 8) {
+        RA -= 1;
+        NO -= 1;
+      }
+      if (jac2_smem_doubles(n, RA, NO) <= ar.fast_cap) {
+        const int64_t ld4 = jac2_ld(n);
+        double* A = ar.take(int64_t(n) * ld4);
+        double* Vt = ar.take(int64_t(n) * ld4);
+        if (n <= 256) return cta_sym_eig_jac2<8>(n, m, vals, vecs, A, Vt, ar.fast, RA, NO);
+        if (n <= 512) return cta_sym_eig_jac2<16>(n, m, vals, vecs, A, Vt, ar.fast, RA, NO);
+        return cta_sym_eig_jac2<24>(n, m, vals, vecs, A, Vt, ar.fast, RA, NO);
+      }
+    }
     if (ar.fast && n >= 48 && blockDim.x == kPipeThreads) {
       int R = 8;
       while (R > 4 && pipelined_smem_doubles(n, R) > ar.fast_cap) R -= 2;

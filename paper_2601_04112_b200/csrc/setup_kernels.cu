@@ -375,7 +375,7 @@ __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
   for (int idx = blockIdx.x * WPB + warp; idx < g.n_list; idx += gridDim.x * WPB) gevp_problem(t, g, idx, ws);
 }
 
-constexpr int64_t kFastCap = 24 * 1024;  // shared doubles for the pipelined Jacobi (192 KiB)
+constexpr int64_t kFastCap = 27000;  // shared doubles for the pipelined Jacobi (211 KiB; + 8 KiB static)
 
 template <bool SMEM>
 __global__ void __launch_bounds__(512) k_gevp_block(GevpArgs g) {
@@ -823,9 +823,12 @@ __global__ void __launch_bounds__(512) k_dense_eig_block(int n, const double* a,
 
 int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, int path, cudaStream_t s) {
   {
-    const char* e = getenv("LSB_EIG_SPLIT");
-    const int split = (e && e[0] == '0') ? 0 : 1;
+    const char* e = getenv("LSB_EIG_SPLIT");  // 1: p/c (default), 2: row-p warps (experimental), 0: pipelined
+    const int split = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
     LSB_CUDA(cudaMemcpyToSymbol(g_eig_split, &split, sizeof(split)));
+    const char* dv = getenv("LSB_JAC2_DBG");
+    const int dbg = dv ? (dv[0] == '2' ? 2 : 1) : 0;
+    LSB_CUDA(cudaMemcpyToSymbol(g_jac2_dbg, &dbg, sizeof(dbg)));
   }
   if (getenv("LSB_EIG_PROF")) {
     static long long* buf = nullptr;
@@ -854,7 +857,7 @@ int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, 
     if (dp) {
       long long h[8];
       LSB_CUDA(cudaMemcpy(h, dp, sizeof(h), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "eig prof (Mcycles): [pipelined: smsum wait+barrier params rotate rowend vapply | p/c: prod-barrier prod-chain cons-prefetch cons-barrier cons-rotate rowend] %.1f %.1f %.1f %.1f %.1f %.1f rotations %lld\n",
+      fprintf(stderr, "eig prof (Mcycles): [jac2: par-wait par-total bulk-wait bulk-total cons-wait cons-total] %.1f %.1f %.1f %.1f %.1f %.1f rotations %lld\n",
               h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6, h[6]);
     }
   }
