@@ -193,9 +193,9 @@ __global__ void k_tiles(const uint64_t* key, const int32_t* head, const int32_t*
   }
 }
 
-constexpr int kTileRows = 16;     // rows of G staged per step
+constexpr int kTileRows = 32;     // rows of G staged per step
 constexpr int kTileThreads = 256;
-constexpr int kSub = 64;          // output sub-tile edge
+constexpr int kSub = 32;          // output sub-tile edge
 
 struct TileArgs {
   const int64_t* goff;  // G_{l+1}
@@ -215,16 +215,6 @@ struct TileArgs {
   int64_t n_items;
 };
 
-__device__ __forceinline__ int64_t lower_bound_col(const int32_t* col, int64_t lo, int64_t hi, int32_t c) {
-  while (lo < hi) {
-    const int64_t mid = (lo + hi) >> 1;
-    if (col[mid] < c)
-      lo = mid + 1;
-    else
-      hi = mid;
-  }
-  return lo;
-}
 
 // One CTA per (tile, sub-tile): stages kTileRows shared rows of the a- and
 // b-segments (dense, with a presence flag = stored entry), then every thread
@@ -260,21 +250,23 @@ __global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
       __syncthreads();
       const int lane = threadIdx.x & 31;
       for (int rr = threadIdx.x >> 5; rr < nr; rr += blockDim.x >> 5) {
+        // one coalesced pass over the row (no dependent binary search)
         const int64_t r = g.rows[rb + rr];
         const int64_t lo = g.goff[r], hi = g.goff[r + 1];
-        const int64_t xa = lower_bound_col(g.gcol, lo, hi, ca);
-        for (int64_t k = xa + lane; k < hi; k += 32) {
-          const int c = g.gcol[k] - ca;
-          if (c >= bi) break;
-          sa[rr][c] = g.gval[k];
-          pa[rr][c] = 1;
-        }
-        const int64_t xb = lower_bound_col(g.gcol, lo, hi, cb);
-        for (int64_t k = xb + lane; k < hi; k += 32) {
-          const int c = g.gcol[k] - cb;
-          if (c >= bj) break;
-          sb[rr][c] = g.gval[k];
-          pb[rr][c] = 1;
+        for (int64_t k = lo + lane; k < hi; k += 32) {
+          const int col = g.gcol[k];
+          const unsigned ea = static_cast<unsigned>(col - ca), eb = static_cast<unsigned>(col - cb);
+          if (ea < static_cast<unsigned>(bi) || eb < static_cast<unsigned>(bj)) {
+            const double v = g.gval[k];
+            if (ea < static_cast<unsigned>(bi)) {
+              sa[rr][ea] = v;
+              pa[rr][ea] = 1;
+            }
+            if (eb < static_cast<unsigned>(bj)) {
+              sb[rr][eb] = v;
+              pb[rr][eb] = 1;
+            }
+          }
         }
       }
       __syncthreads();

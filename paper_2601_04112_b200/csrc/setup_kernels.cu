@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <numeric>
 #include <tuple>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -409,6 +410,8 @@ struct SmArgs {
   int64_t ws_stride;
 };
 
+constexpr int kSmBigSub = 96;  // CTA teams factor subdomains of at least this size warp-parallel
+
 __host__ __device__ inline int64_t sm_ws(int64_t nw, int64_t ng) {
   const int64_t m = nw + ng;
   return r2(8) + 2 * r2(m * m) + r2(nw * m);
@@ -474,6 +477,94 @@ __device__ inline void chol_solve_unit(const double* l, int m, int j, double* x)
   }
 }
 
+// Large blocks (CTA team): the same factorization and inverse columns with a
+// warp per dot product (coalesced rows, fixed xor-tree order). The Schwarz
+// blocks only feed the smoother (solve tolerance), so the
+// reordered sums are deterministic but not the reference's bits.
+__device__ inline double warp_dot(const double* a, const double* b, int n, int lane) {
+  double s0 = 0.0, s1 = 0.0;
+  int k = lane;
+  for (; k + 32 < n; k += 64) {
+    s0 += a[k] * b[k];
+    s1 += a[k + 32] * b[k + 32];
+  }
+  if (k < n) s0 += a[k] * b[k];
+  double s = s0 + s1;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
+__device__ bool cta_cholesky_rows(const BlockTeam& t, double* l, int m, double* slot) {
+  const int warp = t.rank() >> 5, lane = t.rank() & 31, nwarps = t.size() >> 5;
+  for (int j = 0; j < m; ++j) {
+    const double* rj = l + int64_t(j) * m;
+    if (warp == 0) {
+      const double dd = warp_dot(rj, rj, j, lane);
+      if (lane == 0) slot[0] = rj[j] - dd;
+    }
+    t.sync();
+    const double d = slot[0];
+    if (!(d > 0.0)) {
+      t.sync();
+      return false;
+    }
+    const double ljj = sqrt(d);
+    for (int i = j + 1 + warp; i < m; i += nwarps) {
+      double* ri = l + int64_t(i) * m;
+      const double sdot = warp_dot(ri, rj, j, lane);
+      if (lane == 0) ri[j] = (ri[j] - sdot) / ljj;
+    }
+    if (t.rank() == 0) l[int64_t(j) * m + j] = ljj;
+    t.sync();
+  }
+  return true;
+}
+
+__device__ bool cta_factor_spd(const BlockTeam& t, double* blk, const double* orig, int m, double* slot) {
+  if (cta_cholesky_rows(t, blk, m, slot)) return true;
+  if (t.rank() == 0) {
+    double maxd = 0.0;
+    for (int i = 0; i < m; ++i) maxd = fmax(maxd, fabs(orig[int64_t(i) * m + i]));
+    slot[1] = 1e-12 * maxd;
+  }
+  t.sync();
+  const double jitter = slot[1];
+  for (int64_t e = t.rank(); e < int64_t(m) * m; e += t.size())
+    blk[e] = orig[e] + ((e / m == e % m) ? jitter : 0.0);
+  t.sync();
+  return cta_cholesky_rows(t, blk, m, slot);
+}
+
+// columns j < nw of (L Lᵀ)⁻¹, a warp per column: forward over rows of L,
+// backward over rows of Lt = Lᵀ (both contiguous)
+__device__ void cta_inverse_columns(const BlockTeam& t, const double* l, double* lt, int m, int nw, double* X) {
+  const int warp = t.rank() >> 5, lane = t.rank() & 31, nwarps = t.size() >> 5;
+  for (int64_t e = t.rank(); e < int64_t(m) * m; e += t.size()) {
+    const int i = static_cast<int>(e / m), k = static_cast<int>(e % m);
+    lt[int64_t(k) * m + i] = l[e];
+  }
+  t.sync();
+  for (int j = warp; j < nw; j += nwarps) {
+    double* x = X + int64_t(j) * m;
+    for (int i = lane; i < j; i += 32) x[i] = 0.0;
+    __syncwarp();
+    for (int i = j; i < m; ++i) {
+      const double* ri = l + int64_t(i) * m;
+      const double sdot = warp_dot(ri + j, x + j, i - j, lane);
+      if (lane == 0) x[i] = ((i == j ? 1.0 : 0.0) - sdot) / ri[i];
+      __syncwarp();
+    }
+    for (int ii = m - 1; ii >= 0; --ii) {
+      const double* ci = lt + int64_t(ii) * m;
+      const double sdot = warp_dot(ci + ii + 1, x + ii + 1, m - ii - 1, lane);
+      if (lane == 0) x[ii] = (x[ii] - sdot) / ci[ii];
+      __syncwarp();
+    }
+  }
+  t.sync();
+}
+
 template <class Team>
 __device__ void smoother_problem(const Team& t, const SmArgs& g, int idx, double* ws) {
   const int agg = g.list[idx];
@@ -497,12 +588,24 @@ __device__ void smoother_problem(const Team& t, const SmArgs& g, int idx, double
   }
   t.sync();
   t_copy(t, blk, orig, int64_t(m) * m);
-  if (!t_factor_spd(t, blk, orig, m, slot)) {
-    if (t.rank() == 0) g.status[agg] = 1;
-    return;
+  bool big = false;
+  if constexpr (std::is_same<Team, BlockTeam>::value) big = m >= kSmBigSub && t.size() >= 256;
+  if (big) {
+    if constexpr (std::is_same<Team, BlockTeam>::value) {
+      if (!cta_factor_spd(t, blk, orig, m, slot)) {
+        if (t.rank() == 0) g.status[agg] = 1;
+        return;
+      }
+      cta_inverse_columns(t, blk, orig, m, nw, X);  // orig is free now: it holds Lᵀ
+    }
+  } else {
+    if (!t_factor_spd(t, blk, orig, m, slot)) {
+      if (t.rank() == 0) g.status[agg] = 1;
+      return;
+    }
+    for (int j = t.rank(); j < nw; j += t.size()) chol_solve_unit(blk, m, j, X + int64_t(j) * m);
+    t.sync();
   }
-  for (int j = t.rank(); j < nw; j += t.size()) chol_solve_unit(blk, m, j, X + int64_t(j) * m);
-  t.sync();
   double* out = g.sm_data + g.sm_off[agg];
   const int64_t packed = int64_t(nw) * (nw + 1) / 2;
   for (int64_t e = t.rank(); e < packed; e += t.size()) {

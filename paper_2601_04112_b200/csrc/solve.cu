@@ -224,6 +224,64 @@ void schwarz_lane_launch(const SchwarzView& v, int64_t g_begin, int64_t g_end, c
 // warp transaction and each lane has nΩ (RAS) or nω (RAS-T) independent
 // loads in flight. The ω×ω triangle is read by both of its rows (L1 keeps
 // the second read on chip: the rows of a group are consecutive items).
+// Fully unrolled row of a group with the dominant interior shape (NW, NG):
+// every block and residual load of the lane is issued before the first use.
+template <int MODE, int NW, int NG>
+__device__ __forceinline__ double lrow_fixed(const int32_t* __restrict__ ids, const double* __restrict__ blk, int row,
+                                             const double* __restrict__ r) {
+  constexpr int P0 = NW * (NW + 1) / 2;
+  double s0 = 0.0, s1 = 0.0;
+  if (MODE < 2) {
+    double rv[NW + NG], bv[NW + NG];
+#pragma unroll
+    for (int j = 0; j < NW + NG; ++j) {
+      const int id = ids[j * 32];
+      rv[j] = id >= 0 ? __ldg(&r[id]) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      const int lo = row < j ? row : j, hi = row < j ? j : row;
+      const int k = lo * NW - (lo * (lo - 1)) / 2 + (hi - lo);
+      bv[j] = __ldg(&blk[k * 32]);
+    }
+#pragma unroll
+    for (int q = 0; q < NG; ++q) bv[NW + q] = __ldcs(&blk[(P0 + row * NG + q) * 32]);
+#pragma unroll
+    for (int j = 0; j < NW + NG; ++j) {
+      if (j & 1)
+        s1 += bv[j] * rv[j];
+      else
+        s0 += bv[j] * rv[j];
+    }
+  } else {
+    double rv[NW], bv[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      const int id = ids[i * 32];
+      rv[i] = id >= 0 ? __ldg(&r[id]) : 0.0;
+    }
+    if (row < NW) {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) {
+        const int lo = row < i ? row : i, hi = row < i ? i : row;
+        const int k = lo * NW - (lo * (lo - 1)) / 2 + (hi - lo);
+        bv[i] = __ldg(&blk[k * 32]);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NW; ++i) bv[i] = __ldcs(&blk[(P0 + i * NG + (row - NW)) * 32]);
+    }
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      if (i & 1)
+        s1 += bv[i] * rv[i];
+      else
+        s0 += bv[i] * rv[i];
+    }
+  }
+  return s0 + s1;
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) k_schwarz_lrow(SchwarzView v, const int32_t* __restrict__ items, int64_t i0,
                                                       int64_t i1, const double* __restrict__ r,
@@ -238,6 +296,16 @@ __global__ void __launch_bounds__(256) k_schwarz_lrow(SchwarzView v, const int32
     const double* __restrict__ blk = v.lane_blk + v.g_blk_off[g] + lane;
     const int64_t p0 = int64_t(nw) * (nw + 1) / 2;
     const int out = ids[row * 32];
+    if (nw == 9 && ng == 16) {  // 3x3 aggregates with overlap 1 (config 2 interior)
+      const double sum = lrow_fixed<MODE, 9, 16>(ids, blk, row, r);
+      if (out >= 0) {
+        if (MODE == 0)
+          e[out] = sum;
+        else
+          e[out] += sum;
+      }
+      continue;
+    }
     double s0 = 0.0, s1 = 0.0;
     if (MODE < 2) {
 #pragma unroll 4
