@@ -312,16 +312,17 @@ __device__ int cta_sym_eig_pipelined(int n, const double* m, double* vals, doubl
 //     store during rotation 2k+1 (still inside the patch window).
 constexpr int kMaxOwn = 5;  // pairs per consumer thread: n <= 384 * kMaxOwn
 
-template <int R>
+template <int R, int NCW = 12>
 __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs, double* A, double* Vt, double* sm) {
   // Warp 0 (SMSP 0) produces; warps 4, 8, 12 idle so SMSP 0 issues only the
   // producer's dependent chain; the other 12 warps consume.
-  constexpr int D = R - 2, NL = 2 * R, PS = R + 1, T = kPipeThreads, NC = 384, QN = 64;
+  // NCW = 12: warps 4, 8, 12 idle; NCW = 15: every warp but the producer consumes
+  constexpr int D = R - 2, NL = 2 * R, PS = R + 1, T = kPipeThreads, NC = NCW * 32, QN = 64;
   const int tid = threadIdx.x;
   const int wid = tid >> 5;
   const bool producer = wid == 0;
-  const bool idle = (wid & 3) == 0 && wid != 0;
-  const int ctid = (wid - 1 - (wid >> 2)) * 32 + (tid & 31);  // consumer index 0..383
+  const bool idle = NCW == 12 && (wid & 3) == 0 && wid != 0;
+  const int ctid = (NCW == 12 ? wid - 1 - (wid >> 2) : wid - 1) * 32 + (tid & 31);  // consumer index 0..383
   const int64_t ld = (n + 1) & ~int64_t(1);
   double* pvs = sm;                      // a(p,·) at row start / hand-offs
   double* vp = pvs + ld;                 // Vᵀ row p at row start
@@ -368,7 +369,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
   long long base = 0;
   bool converged = false;
   long long* const prof = g_eig_prof;  // optional cycle counters (test hook)
-  long long c_w = 0, c_c = 0, c_b = 0, c_p = 0, c_r = 0, c_e = 0, c_n = 0;
+  long long c_w = 0, c_c = 0, c_b = 0, c_p = 0, c_r = 0, c_e = 0, c_n = 0, c_rot = 0;
   for (int sweep = 0; sweep < 64; ++sweep) {
     double smv = 0.0;
     for (int p = 0; p + 1 < n; ++p) {
@@ -458,6 +459,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
             c_c += k2 - k1;
             c_w += clock64() - k2;
             ++c_n;
+            c_rot += prot;
           }
         }
         if (tid == 0) {
@@ -631,6 +633,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[1]), c_c);
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[5]), c_e);
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[6]), c_n);
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[7]), c_rot);
     }
     if (tid == 32) {
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[2]), c_b);
@@ -655,11 +658,16 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
 
 #include "jacobi2.cuh"
 
-__device__ int g_eig_split = 1;
+__device__ int g_eig_split = 3;
   // 1: producer/consumer, 0: one barrier per rotation (test hook)
 
 __device__ __noinline__ int cta_sym_eig_pipelined_any(int n, const double* m, double* vals, double* vecs, double* A,
                                                 double* Vt, double* sm, int R) {
+  if (g_eig_split == 3 && n <= 384 * kMaxOwn) {
+    if (R >= 8) return cta_sym_eig_pc<8, 15>(n, m, vals, vecs, A, Vt, sm);
+    if (R >= 6) return cta_sym_eig_pc<6, 15>(n, m, vals, vecs, A, Vt, sm);
+    return cta_sym_eig_pc<4, 15>(n, m, vals, vecs, A, Vt, sm);
+  }
   if (g_eig_split && n <= 384 * kMaxOwn) {
     if (R >= 8) return cta_sym_eig_pc<8>(n, m, vals, vecs, A, Vt, sm);
     if (R >= 6) return cta_sym_eig_pc<6>(n, m, vals, vecs, A, Vt, sm);

@@ -926,8 +926,9 @@ __global__ void __launch_bounds__(512) k_dense_eig_block(int n, const double* a,
 
 int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, int path, cudaStream_t s) {
   {
-    const char* e = getenv("LSB_EIG_SPLIT");  // 1: p/c (default), 2: row-p warps (experimental), 0: pipelined
-    const int split = (e && e[0] >= '0' && e[0] <= '2') ? e[0] - '0' : 1;
+    // 3: p/c with 15 consumer warps (default), 1: p/c with 12, 2: row-p warps (experimental), 0: pipelined
+    const char* e = getenv("LSB_EIG_SPLIT");
+    const int split = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
     LSB_CUDA(cudaMemcpyToSymbol(g_eig_split, &split, sizeof(split)));
     const char* dv = getenv("LSB_JAC2_DBG");
     const int dbg = dv ? (dv[0] == '2' ? 2 : 1) : 0;
@@ -960,8 +961,8 @@ int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, 
     if (dp) {
       long long h[8];
       LSB_CUDA(cudaMemcpy(h, dp, sizeof(h), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "eig prof (Mcycles): [jac2: par-wait par-total bulk-wait bulk-total cons-wait cons-total] %.1f %.1f %.1f %.1f %.1f %.1f rotations %lld\n",
-              h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6, h[6]);
+      fprintf(stderr, "eig prof (Mcycles): %.1f %.1f %.1f %.1f %.1f %.1f steps %lld rounds %lld\n",
+              h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6, h[6], h[7]);
     }
   }
   const auto hv = vals.download(s);
@@ -1110,6 +1111,12 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_bad, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
   }
   const bool prof_on = getenv("LSB_GEVP_PROF") != nullptr;
+  DBuf<long long> eprof(prof_on ? 8 : 1, s);
+  if (prof_on) {
+    eprof.zero(s);
+    long long* ep = eprof.get();
+    LSB_CUDA(cudaMemcpyToSymbol(g_eig_prof, &ep, sizeof(ep)));
+  }
   DBuf<long long> gprof(prof_on ? na * 6 : 1, s);
   if (prof_on) {
     gprof.zero(s);
@@ -1224,6 +1231,9 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
             sm[1] / 1e6, mx[2] / 1e6, sm[2] / 1e6, mx[3] / 1e6, sm[3] / 1e6, mx[4] / 1e6, sm[4] / 1e6);
     long long* np = nullptr;
     LSB_CUDA(cudaMemcpyToSymbol(g_gevp_prof, &np, sizeof(np)));
+    const auto he = eprof.download(s);
+    fprintf(stderr, "   large-n Jacobi steps %lld, rotations %lld\n", he[6], he[7]);
+    LSB_CUDA(cudaMemcpyToSymbol(g_eig_prof, &np, sizeof(np)));
   }
   if (getenv("LSB_GRAM_CHECK") && pre.get()) {
     unsigned long long hb[8];
