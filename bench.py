@@ -324,10 +324,10 @@ def main() -> None:
         tp = os.path.join(ROOT, "profiles", "schwarz_traffic.json")
         if os.path.exists(tp):
             with open(tp) as f:
-                traffic = json.load(f).get("dram_bytes_per_sweep_pair")
+                traffic = json.load(f).get("dram_bytes_per_launch")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                    "kernel": "level-0 Schwarz RAS + RAS-T sweep pair (k_schwarz_warp)",
+                    "kernel": "level-0 Schwarz RAS + RAS-T sweep pair (k_schwarz_lrow: 1 RAS + 4 colour launches)",
                     "bytes_per_launch": ks.schwarz_bytes / max(ks.schwarz_launches, 1),
                     "peak_source": peaks["source"]}
 
