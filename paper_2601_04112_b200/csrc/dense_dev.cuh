@@ -335,6 +335,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
   __shared__ unsigned pmask[NL];
   __shared__ double q_s[QN], q_tau[QN], q_piv[QN], q_ny[QN];
   __shared__ int q_rot[QN];
+  __shared__ int q_first;  // first rotating step of the current row
   for (int64_t e = tid; e < int64_t(n) * n; e += T) {  // full symmetric copy (eigen.hpp:44)
     const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
     double val = m[e];
@@ -393,19 +394,39 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
         vp[j] = Vt[int64_t(p) * ld + j];
       }
       if (tid < NL) pmask[tid] = 0u;
+      if (tid == 0) q_first = n;
       __syncthreads();
+      // Steps before the row's first rotation see the row as loaded: find that
+      // step with the reference's predicates (eigen.hpp:62-65) in parallel,
+      // apply the "zeroed" pairs before it, and start the pipeline there.
+      {
+        const double dp0 = d[p];
+        for (int q = p + 1 + tid; q < n; q += T) {
+          const double a = pvs[q], g = 100.0 * fabs(a), dq = d[q];
+          const bool zero = sweep > 3 && fabs(dp0) + g == fabs(dp0) && fabs(dq) + g == fabs(dq);
+          if (!zero && fabs(a) > tresh) atomicMin(&q_first, q);
+        }
+        __syncthreads();
+        const int q1 = q_first;
+        for (int q = p + 1 + tid; q < q1; q += T) {
+          const double a = pvs[q], g = 100.0 * fabs(a), dq = d[q];
+          if (sweep > 3 && fabs(dp0) + g == fabs(dp0) && fabs(dq) + g == fabs(dq)) pvs[q] = 0.0;
+        }
+        __syncthreads();
+      }
+      const int q_start = q_first;
       if (producer) {
         // all 32 lanes walk the rounds (bar.sync is warp-aligned); lane 0 computes
         double dp = d[p], zp = z[p];
         double ps = 0.0, ptau = 0.0, ph = 0.0;
         int prot = 0;
         double ny_prev = 0.0;
-        for (int q = p + 1; q < n; ++q) {
+        for (int q = q_start; q < n; ++q) {
           const long long t = base + (q - p - 1);
           const long long k1 = prof ? clock64() : 0;
           if (tid == 0) {
             double apq = pvs[q];  // a(p,q) after the consumers' rotations <= q-2 (hand-off)
-            if (q > p + 1) {
+            if (q > q_start) {
               if (prot) {  // rotation q-1 on pair q; the owner of q-1 stores a(q-1,q) at rotation q
                 const int pq = q - 1;
                 const double hy = ring[int64_t(2 * (pq % R)) * ld + q];
@@ -481,8 +502,8 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
           pend[k] = 0.0;
         }
         int pend_q = -1;  // rotation whose mirror stores are held back
-        for (int k = 1; k <= D; ++k) prefetch(p + k);
-        for (int q = p + 1; q < n; ++q) {
+        for (int k = 0; k < D; ++k) prefetch(q_start + k);
+        for (int q = q_start; q < n; ++q) {
           const long long t = base + (q - p - 1);
           const long long k0 = prof ? clock64() : 0;
           prefetch(q + D);
@@ -531,14 +552,14 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
               }
               continue;
             }
-            if (j == q - 1 && j > p) pr[k] = q_piv[qp];  // the pivot of rotation q-1 resumes
+            if (j == q - 1 && j >= q_start) pr[k] = q_piv[qp];  // the pivot of rotation q-1 resumes
             const bool held = held_q && j != p && j != q - 1 && j != q;
             if (rot) {
               const double vx = vr[k], vy = qvv[j];
               vr[k] = vx - s * (vy + vx * tau);
               vrow[j] = vy + s * (vx - vy * tau);
             }
-            const bool prev_rot = j == q - 1 && j > p && q_rot[qp] != 0;  // a(q,q-1) from the producer
+            const bool prev_rot = j == q - 1 && j >= q_start && q_rot[qp] != 0;  // a(q,q-1) from the producer
             if (!rot || j == p || j == q || j == q + 1) {
               if (held) mir[q - 1] = pend[k];
               if (prev_rot) {
@@ -603,7 +624,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
         for (int k = 0; k < kMaxOwn; ++k) {
           const int j = ctid + k * NC;
           if (j < n) {
-            pvs[j] = (j == n - 1 && j > p) ? piv_last : pr[k];
+            pvs[j] = (j == n - 1 && j > p && q_start < n) ? piv_last : pr[k];
             vp[j] = vr[k];
           }
         }
