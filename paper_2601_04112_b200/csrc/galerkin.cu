@@ -143,13 +143,23 @@ __global__ void __launch_bounds__(kGpWarps * 32) k_gp(GpArgs g) {
 
 // (agg, row) pairs of the row sets re-sorted by row: every G row's hit
 // aggregates in ascending order
+// one thread per (aggregate, row) pair; the aggregate by binary search in
+// nz_off (deep levels have few aggregates with millions of rows each)
 __global__ void k_rs_pairs(const int64_t* nz_off, const int32_t* nz, int64_t n_agg, uint32_t* key_row,
                            int32_t* val_agg) {
-  for (int64_t a = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; a < n_agg; a += int64_t(gridDim.x) * blockDim.x)
-    for (int64_t p = nz_off[a]; p < nz_off[a + 1]; ++p) {
-      key_row[p] = static_cast<uint32_t>(nz[p]);
-      val_agg[p] = static_cast<int32_t>(a);
+  const int64_t total = nz_off[n_agg];
+  for (int64_t p = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; p < total; p += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = n_agg - 1;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (nz_off[mid] <= p)
+        lo = mid;
+      else
+        hi = mid - 1;
     }
+    key_row[p] = static_cast<uint32_t>(nz[p]);
+    val_agg[p] = static_cast<int32_t>(lo);
+  }
 }
 
 __global__ void k_mult_to_cnt(const int32_t* mult, int64_t m, int64_t* c) {
@@ -220,11 +230,18 @@ struct TileArgs {
 // b-segments (dense, with a presence flag = stored entry), then every thread
 // advances its outputs over those rows in ascending order.
 __global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
+  // Segments are staged dense (absent entries = +0: adding the ±0 products
+  // leaves every sum unchanged, it starts at +0 and never becomes -0) with a
+  // presence mask per row; an output exists in the Symbolic pattern iff some
+  // row holds both of its entries.
+  static_assert(kSub == 32, "presence masks are 32-bit");
   __shared__ double sa[kTileRows][kSub];
   __shared__ double sb[kTileRows][kSub];
-  __shared__ uint8_t pa[kTileRows][kSub];
-  __shared__ uint8_t pb[kTileRows][kSub];
+  __shared__ unsigned ma[kTileRows], mb[kTileRows];
   constexpr int kPer = kSub * kSub / kTileThreads;
+  constexpr int kIStep = kTileThreads / kSub;  // output rows of a thread: i0 + kIStep*q, column j
+  const int lane = threadIdx.x & 31;
+  const int ti = threadIdx.x / kSub, tj = threadIdx.x % kSub;
   for (int64_t w = blockIdx.x; w < g.n_items; w += gridDim.x) {
     const int t = g.wi_tile[w];
     const int i0 = g.wi_i0[w], j0 = g.wi_j0[w];
@@ -234,25 +251,26 @@ __global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
     const int bi = min(kSub, ka - i0), bj = min(kSub, kb - j0);
     const int64_t r0 = g.tstart[t], r1 = g.tstart[t + 1];
     double acc[kPer];
-    bool touched[kPer];
+    unsigned touched = 0u;
 #pragma unroll
-    for (int q = 0; q < kPer; ++q) {
-      acc[q] = 0.0;
-      touched[q] = false;
-    }
+    for (int q = 0; q < kPer; ++q) acc[q] = 0.0;
     for (int64_t rb = r0; rb < r1; rb += kTileRows) {
       const int nr = static_cast<int>(r1 - rb < kTileRows ? r1 - rb : kTileRows);
-      for (int q = threadIdx.x; q < kTileRows * kSub; q += blockDim.x) {
+      for (int q = threadIdx.x; q < nr * kSub; q += blockDim.x) {  // outputs beyond bi/bj are discarded
         const int rr = q / kSub, c = q % kSub;
-        pa[rr][c] = 0;
-        pb[rr][c] = 0;
+        if (c < bi) sa[rr][c] = 0.0;
+        if (c < bj) sb[rr][c] = 0.0;
+      }
+      if (threadIdx.x < kTileRows) {
+        ma[threadIdx.x] = 0u;
+        mb[threadIdx.x] = 0u;
       }
       __syncthreads();
-      const int lane = threadIdx.x & 31;
       for (int rr = threadIdx.x >> 5; rr < nr; rr += blockDim.x >> 5) {
-        // one coalesced pass over the row (no dependent binary search)
+        // one coalesced pass over the row
         const int64_t r = g.rows[rb + rr];
         const int64_t lo = g.goff[r], hi = g.goff[r + 1];
+        unsigned bits_a = 0u, bits_b = 0u;
         for (int64_t k = lo + lane; k < hi; k += 32) {
           const int col = g.gcol[k];
           const unsigned ea = static_cast<unsigned>(col - ca), eb = static_cast<unsigned>(col - cb);
@@ -260,30 +278,35 @@ __global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
             const double v = g.gval[k];
             if (ea < static_cast<unsigned>(bi)) {
               sa[rr][ea] = v;
-              pa[rr][ea] = 1;
+              bits_a |= 1u << ea;
             }
             if (eb < static_cast<unsigned>(bj)) {
               sb[rr][eb] = v;
-              pb[rr][eb] = 1;
+              bits_b |= 1u << eb;
             }
           }
         }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          bits_a |= __shfl_xor_sync(0xffffffffu, bits_a, o);
+          bits_b |= __shfl_xor_sync(0xffffffffu, bits_b, o);
+        }
+        if (lane == 0) {
+          ma[rr] = bits_a;
+          mb[rr] = bits_b;
+        }
       }
       __syncthreads();
+      for (int rr = 0; rr < nr; ++rr) {
+        const unsigned am = ma[rr];
+        const double yb = sb[rr][tj];
+        const bool hb = ((mb[rr] >> tj) & 1u) != 0u;
 #pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const int o = threadIdx.x + q * kTileThreads;
-        const int i = o / kSub, j = o % kSub;
-        if (i >= bi || j >= bj) continue;
-        double s = acc[q];
-        bool tt = touched[q];
-        for (int rr = 0; rr < nr; ++rr)
-          if (pa[rr][i] && pb[rr][j]) {
-            s += sa[rr][i] * sb[rr][j];
-            tt = true;
-          }
-        acc[q] = s;
-        touched[q] = tt;
+        for (int q = 0; q < kPer; ++q) {
+          const int i = ti + kIStep * q;
+          acc[q] += sa[rr][i] * yb;
+          if (hb && ((am >> i) & 1u)) touched |= 1u << q;
+        }
       }
       __syncthreads();
     }
@@ -291,12 +314,11 @@ __global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
     uint8_t* tm = g.tmask + g.tval_off[t];
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
-      const int o = threadIdx.x + q * kTileThreads;
-      const int i = o / kSub, j = o % kSub;
+      const int i = ti + kIStep * q, j = tj;
       if (i >= bi || j >= bj) continue;
       const int64_t e = int64_t(i0 + i) * kb + (j0 + j);
       tv[e] = acc[q];
-      tm[e] = touched[q] ? 1 : 0;
+      tm[e] = ((touched >> q) & 1u) ? 1 : 0;
     }
     __syncthreads();
   }
@@ -397,7 +419,7 @@ void galerkin_gtg(const DevCsr& gn, const DevRowSets& rs, int64_t n_agg, const D
   {
     DBuf<uint32_t> k1(std::max<int64_t>(npairs, 1), s), k2(std::max<int64_t>(npairs, 1), s);
     DBuf<int32_t> v1(std::max<int64_t>(npairs, 1), s);
-    k_rs_pairs<<<grid_for(n_agg), kThreads, 0, s>>>(rs.nz_off.get(), rs.nz.get(), n_agg, k1.get(), v1.get());
+    k_rs_pairs<<<grid_for(npairs), kThreads, 0, s>>>(rs.nz_off.get(), rs.nz.get(), n_agg, k1.get(), v1.get());
     LSB_LAUNCH();
     size_t tmp = 0;
     const int eb = bits_for(static_cast<uint64_t>(m));
