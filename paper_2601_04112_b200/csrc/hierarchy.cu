@@ -359,6 +359,15 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
   h->ratios.assign(p->coarsening_ratios, p->coarsening_ratios + p->n_ratios);
   h->device = p->device;
   LSB_CUDA(cudaSetDevice(p->device));
+  {
+    // Keep freed stream-ordered memory mapped in the device pool: the setup
+    // allocates and frees hundreds of MB of per-level workspace, and returning
+    // it to the driver at every synchronisation costs seconds of remapping.
+    cudaMemPool_t pool;
+    LSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, p->device));
+    uint64_t keep = UINT64_MAX;
+    LSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
   LSB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   cudaStream_t s = h->stream;
   auto stage = [&](const char* name, Clock::time_point t0) {
