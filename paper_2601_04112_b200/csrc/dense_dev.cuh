@@ -370,7 +370,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
   long long base = 0;
   bool converged = false;
   long long* const prof = g_eig_prof;  // optional cycle counters (test hook)
-  long long c_w = 0, c_c = 0, c_b = 0, c_p = 0, c_r = 0, c_e = 0, c_n = 0, c_rot = 0;
+  long long c_w = 0, c_c = 0, c_b = 0, c_p = 0, c_r = 0, c_e = 0, c_n = 0, c_rot = 0, c_skip = 0;
   for (int sweep = 0; sweep < 64; ++sweep) {
     double smv = 0.0;
     for (int p = 0; p + 1 < n; ++p) {
@@ -608,6 +608,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
             c_b += k1 - k0;
             c_p += k2 - k1;
             c_r += k3 - k2;
+            if (!rot) c_skip += k3 - k0;  // whole step time of non-rotating steps
           }
         }
         cp_async_wait<0>();
@@ -657,6 +658,7 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[7]), c_rot);
     }
     if (tid == 32) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(&prof[0]), c_skip);
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[2]), c_b);
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[3]), c_p);
       atomicAdd(reinterpret_cast<unsigned long long*>(&prof[4]), c_r);
