@@ -376,7 +376,9 @@ __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
   for (int idx = blockIdx.x * WPB + warp; idx < g.n_list; idx += gridDim.x * WPB) gevp_problem(t, g, idx, ws);
 }
 
-constexpr int64_t kFastCap = 27000;  // shared doubles for the pipelined Jacobi (211 KiB; + 8 KiB static)
+// shared doubles for the pipelined Jacobi: 207 KiB dynamic + the kernels'
+// static shared arrays (15 KiB) stay within the 227 KiB per CTA
+constexpr int64_t kFastCap = 26500;
 
 template <bool SMEM>
 __global__ void __launch_bounds__(512) k_gevp_block(GevpArgs g) {
@@ -1109,6 +1111,10 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     unsigned long long z[8] = {0};
     LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_check, &chk, sizeof(chk), 0, cudaMemcpyHostToDevice, s));
     LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_bad, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
+  }
+  if (const char* e = getenv("LSB_EIG_SPLIT")) {  // Jacobi schedule override (experiments)
+    const int split = (e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
+    LSB_CUDA(cudaMemcpyToSymbolAsync(g_eig_split, &split, sizeof(split), 0, cudaMemcpyHostToDevice, s));
   }
   const bool prof_on = getenv("LSB_GEVP_PROF") != nullptr;
   DBuf<long long> eprof(prof_on ? 8 : 1, s);
