@@ -116,7 +116,10 @@ def dist_setup(n_gpus: int):
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl")
+        import torch
+
+        # NCCL between the GPUs of the box; gloo only for the CPU tests of this plumbing
+        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
         pg = dist
     return world, rank, local, pg
 
@@ -140,7 +143,8 @@ def run_reference(args) -> dict:
         chk, kind = refbind.reference(), "reference"
     except FileNotFoundError:
         chk, kind = refbind.oracle(), "port"
-    cfg = configs.config("c2", SAMPLE_GRID)
+    grid = args.sample_grid
+    cfg = configs.config("c2", grid)
     p = refbind.params_for(cfg)
     threads = max(1, min(os.cpu_count() or 1, 64))
 
@@ -166,10 +170,10 @@ def run_reference(args) -> dict:
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c2", "grid": SAMPLE_GRID, "n": cfg.n, "sample_of": "c2 1024x1024",
+        "config": {"workload": "c2", "grid": grid, "n": cfg.n, "sample_of": "c2 1024x1024",
                    "parallelism": f"{threads} independent single-threaded solves"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"config-2 generator at {SAMPLE_GRID}x{SAMPLE_GRID} (n={cfg.n}), setup+PCG end to end, "
+                         "sample": f"config-2 generator at {grid}x{grid} (n={cfg.n}), setup+PCG end to end, "
                                    f"one per thread on {threads} threads"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -204,11 +208,14 @@ def main() -> None:
     ap.add_argument("--config", default="c2")
     ap.add_argument("--grid", type=int, default=None, help="override the grid (debug only; not a bench number)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sample-grid", type=int, default=SAMPLE_GRID,
+                    help="grid of the CPU reference sample (the default is the documented bench sample)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
     world, rank, local, pg = dist_setup(args.gpus)
     if args.impl == "reference":
+        # the reference is a CPU library: rank 0 alone runs it, the other ranks exit 0
         if rank == 0:
             print(json.dumps(run_reference(args)), flush=True)
         return
