@@ -248,11 +248,79 @@ def rotated_aniso_3d(nn: int, eps: float, alpha: float, beta: float):
     return rowptr, cc, vv, m
 
 
-def config(name: str, scale: int | None = None) -> ConfigInput:
-    """Build config ``c1``..``c3``/``c5`` (BASELINE.json configs[0..4]).
+ANNULUS_R0, ANNULUS_R1 = 0.5, 1.0
+ANNULUS_MODES = 4
+
+
+def annulus_field(n_phi: int, n_r: int, seed: int = 3, amplitude: float = 0.05):
+    """Unit field b = (b_r, b_φ) of config 4 on the annulus nodes.
+
+    Closed circular field lines (b = e_φ) with a smooth seeded radial
+    perturbation p(r, φ) = amplitude · Σ_k a_k sin(kφ + ψ_k) · sin(π(r−r0)/(r1−r0))
+    / Σ_k |a_k|, k = 1..4, so |p| ≤ amplitude and p vanishes on both
+    Dirichlet circles; a_k ∈ uniform[-1,1), ψ_k = π·(u_k + 1) with u_k the
+    next draw, all from std::mt19937_64(seed) (the RHS recipe of
+    lsamgdd_cli.cpp:103-107). b = (p, 1)/√(1+p²). Nodes are lexicographic
+    j·n_phi + i (i the periodic angle index, j the radial index); radii are
+    interior nodes r_j = r0 + (j+1)·Δr, Δr = (r1−r0)/(n_r+1), angles φ_i = i·Δφ.
+    """
+    draws = mt19937_64_uniform(seed, 2 * ANNULUS_MODES)
+    a = draws[0::2]
+    psi = math.pi * (draws[1::2] + 1.0)
+    dr = (ANNULUS_R1 - ANNULUS_R0) / (n_r + 1)
+    dphi = 2.0 * math.pi / n_phi
+    r = ANNULUS_R0 + (np.arange(n_r, dtype=np.float64) + 1.0) * dr
+    phi = np.arange(n_phi, dtype=np.float64) * dphi
+    ang = np.zeros(n_phi)
+    for k in range(ANNULUS_MODES):
+        ang += a[k] * np.sin((k + 1) * phi + psi[k])
+    ang *= amplitude / np.abs(a).sum()
+    bump = np.sin(math.pi * (r - ANNULUS_R0) / (ANNULUS_R1 - ANNULUS_R0))
+    p = bump[:, None] * ang[None, :]  # [n_r, n_phi]
+    norm = np.sqrt(1.0 + p * p)
+    return p / norm, 1.0 / norm, r, dr, dphi
+
+
+def annulus_heat(n_phi: int, n_r: int, eps_perp: float, seed: int = 3):
+    """Config 4 factor: G = [√D1; D2^{-1/2}·B], D1 = ε⊥·h²·I, D2 = I, so
+    A = GᵀG = D1 + BᵀD2⁻¹B (BASELINE.json configs[3]).
+
+    B is the first-order upwinded directional derivative b·∇u =
+    b_r ∂u/∂r + (b_φ/r) ∂u/∂φ: the angular part is a backward difference
+    (b_φ > 0 everywhere) that wraps periodically, the radial part a backward
+    difference where b_r ≥ 0 and a forward one where b_r < 0, with
+    homogeneous Dirichlet closure on both circles (the missing neighbour is
+    dropped). h = Δr. Rows 0..n−1 are √D1, rows n..2n−1 are B; m = 2n and
+    every B row touches at most three nodes.
+    """
+    if n_phi < 2 or n_r < 1:
+        raise ValueError("annulus_heat: need n_phi >= 2 and n_r >= 1")
+    br, bphi, r, dr, dphi = annulus_field(n_phi, n_r, seed)
+    n = n_phi * n_r
+    node = np.arange(n, dtype=np.int64)
+    j, i = np.divmod(node, n_phi)
+    br, bphi = br.ravel(), bphi.ravel()
+    c_phi = bphi / (r[j] * dphi)
+    c_r = br / dr
+    west = j * n_phi + (i - 1) % n_phi
+    up = br >= 0.0
+    has_in = up & (j > 0)
+    has_out = ~up & (j + 1 < n_r)
+    rb = n + node
+    rows = [node, rb, rb, rb[has_in], rb[has_out]]
+    cols = [node, node, west, node[has_in] - n_phi, node[has_out] + n_phi]
+    vals = [np.full(n, math.sqrt(eps_perp) * dr), c_phi + np.abs(c_r), -c_phi, -c_r[has_in], c_r[has_out]]
+    m = 2 * n
+    rowptr, cc, vv = _assemble_rows(m, np.concatenate(rows), np.concatenate(cols), np.concatenate(vals), n)
+    return rowptr, cc, vv, m
+
+
+def config(name: str, scale: int | None = None, eps_perp: float = 1e-6) -> ConfigInput:
+    """Build config ``c1``..``c5`` (BASELINE.json configs[0..4]).
 
     ``scale`` overrides the grid edge for parity tests at sizes the oracle
-    finishes in seconds; the bench always uses the full size.
+    finishes in seconds; the bench always uses the full size. ``eps_perp``
+    picks the point of config 4's ε⊥ sweep {1e-3, 1e-6, 1e-9}.
     """
     name = name.lower()
     if name == "c1":
@@ -285,6 +353,17 @@ def config(name: str, scale: int | None = None) -> ConfigInput:
             "c3", nx * nx, rp, c, v, rhs, part, nagg,
             params=dict(thresh_override=20.0, level0_overlap=2),
             meta=dict(grid=nx, eps=1e-6, theta=theta, blocks="8x8", overlap=2, tau=0.05, ref_thresh=20.0, seed=2),
+        )
+    if name == "c4":
+        nx = scale or 2048
+        rp, c, v, m = annulus_heat(nx, nx, eps_perp, seed=3)
+        part, nagg = block_partition_2d(nx, nx, 6, 6)
+        rhs = mt19937_64_uniform(3, nx * nx + 2 * ANNULUS_MODES)[2 * ANNULUS_MODES:]
+        return ConfigInput(
+            "c4", nx * nx, rp, c, v, rhs, part, nagg,
+            params=dict(level0_overlap=2),
+            meta=dict(grid=nx, eps_perp=eps_perp, r0=ANNULUS_R0, r1=ANNULUS_R1, perturbation=0.05,
+                      blocks="6x6", overlap=2, seed=3),
         )
     if name == "c5":
         nn = scale or 256

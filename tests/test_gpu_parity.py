@@ -62,31 +62,47 @@ CASES = [
     ("c2", 128, {}),
     ("c3", 32, {"thresh_override": 0.0}),
     ("c3", 64, {"thresh_override": 10.0}),
+    ("c4", 24, {}),
+    ("c4", 48, {}),
+    ("c4", 30, {"eps_perp": 1e-3}),
+    ("c4", 30, {"eps_perp": 1e-9}),
 ]
+
+
+def _config(name, scale, over):
+    """configs.config for a CASES row; ``eps_perp`` picks config 4's sweep point."""
+    over = dict(over)
+    eps = over.pop("eps_perp", None)
+    cfg = configs.config(name, scale) if eps is None else configs.config(name, scale, eps_perp=eps)
+    return cfg, over
+
+
+def _key(name, scale, over):
+    return (name, scale, tuple(sorted(over.items())))
 
 
 @pytest.fixture(scope="module")
 def built():
     out = {}
     orc = refbind.oracle()
-    for name, scale, over in CASES:
-        cfg = configs.config(name, scale)
+    for name, scale, over0 in CASES:
+        cfg, over = _config(name, scale, over0)
         h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg, keep_spectra=True, **over))
         ho = orc.setup(cfg, refbind.params_for(cfg, keep_spectra=1, **over))
-        out[(name, scale)] = (cfg, h, ho)
+        out[_key(name, scale, over0)] = (cfg, h, ho)
     return out
 
 
 @pytest.mark.parametrize("name,scale,over", CASES)
 def test_hierarchy_bit_exact(gpu, built, name, scale, over):
-    cfg, h, ho = built[(name, scale)]
+    cfg, h, ho = built[_key(name, scale, over)]
     assert_hierarchy_bit_exact(h, ho)
     assert lsamgdd.operator_complexity(h) == ho.operator_complexity()
 
 
 @pytest.mark.parametrize("name,scale,over", CASES)
 def test_vcycle_and_pcg(gpu, built, name, scale, over):
-    cfg, h, ho = built[(name, scale)]
+    cfg, h, ho = built[_key(name, scale, over)]
     r = cfg.rhs
     e, eo = lsamgdd.vcycle(h, r), ho.vcycle(r)
     assert np.linalg.norm(e - eo) <= VCYCLE_RTOL * np.linalg.norm(eo)
@@ -101,9 +117,9 @@ def test_vcycle_and_pcg(gpu, built, name, scale, over):
     assert rep.avg_conv_factor == pytest.approx(rho, rel=1e-12)
 
 
-@pytest.mark.parametrize("name,scale,over", CASES[:3])
+@pytest.mark.parametrize("name,scale,over", CASES[:3] + [CASES[6]])
 def test_schwarz_apply(gpu, built, name, scale, over):
-    cfg, h, ho = built[(name, scale)]
+    cfg, h, ho = built[_key(name, scale, over)]
     rng = np.random.default_rng(5)
     for l in range(h.num_levels - 1):
         r = rng.uniform(-1, 1, h.summary[l].dim)
@@ -113,9 +129,9 @@ def test_schwarz_apply(gpu, built, name, scale, over):
             assert np.linalg.norm(y - yo) <= SCHWARZ_RTOL * np.linalg.norm(yo), (l, mode)
 
 
-@pytest.mark.parametrize("name,scale,over", CASES[:3])
+@pytest.mark.parametrize("name,scale,over", CASES[:3] + [CASES[6]])
 def test_level_spmv_bit_exact(gpu, built, name, scale, over):
-    cfg, h, ho = built[(name, scale)]
+    cfg, h, ho = built[_key(name, scale, over)]
     rng = np.random.default_rng(6)
     for l in range(h.num_levels - 1):
         n = h.summary[l].dim

@@ -189,12 +189,14 @@ def test_setup_input_errors(oracle_lib):
 # ---- oracle == compiled reference, bit for bit -------------------------------------------------
 
 _CASES = [("c1", None, {}), ("c2", 32, {}), ("c2", 64, {}), ("c3", 32, {"thresh_override": 0.0}),
-          ("c3", 64, {"thresh_override": 10.0})]
+          ("c3", 64, {"thresh_override": 10.0}), ("c4", 24, {}), ("c4", 48, {}),
+          ("c4", 30, {"eps_perp": 1e-3}), ("c4", 30, {"eps_perp": 1e-9})]
 
 
 @pytest.mark.parametrize("name,scale,over", _CASES)
 def test_oracle_matches_reference_bitwise(ref_lib, oracle_lib, name, scale, over):
-    cfg = configs.config(name, scale)
+    over = dict(over)
+    cfg = configs.config(name, scale, **({"eps_perp": over.pop("eps_perp")} if "eps_perp" in over else {}))
     p = refbind.params_for(cfg, keep_spectra=1, **over)
     hr = ref_lib.setup(cfg, p)
     ho = oracle_lib.setup(cfg, p)
