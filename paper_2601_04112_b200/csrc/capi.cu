@@ -251,7 +251,7 @@ int lsamgdd_level_spmv(const void* handle, int64_t level, int32_t what, int32_t 
       const int64_t nout = transpose ? iv.n_coarse : iv.n_fine;
       with_vectors(ws, x, nin, y, nout, memory, [&](const double* dx, double* dy) {
         if (transpose) {
-          restrict_pt(iv, dx, dy, ws.s);
+          restrict_pt(iv, dx, dy, ws.s, /*exact=*/true);
         } else {
           LSB_CUDA(cudaMemsetAsync(dy, 0, nout * 8, ws.s));
           prolong_add(iv, dx, dy, ws.s);

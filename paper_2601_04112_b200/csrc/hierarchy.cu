@@ -589,8 +589,10 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
   //   [vcycle(r)->z, rz_next, beta, p = z + beta p]
   //   gp = G p, ap = Gᵀ gp, <p,ap>, alpha, x += αp, r -= α·ap, ‖r‖²
   auto tail = [&]() {
+    if (ws.timing) LSB_CUDA(cudaEventRecordWithFlags(ws.ev[4], s, cudaEventRecordExternal));
     sell_spmv(g, p.get(), gp.get(), nullptr, s);
     pcg_ap_dot(gt, gp.get(), p.get(), ap.get(), ws.red, sc.get(), s);
+    if (ws.timing) LSB_CUDA(cudaEventRecordWithFlags(ws.ev[5], s, cudaEventRecordExternal));
     pcg_update_xr(ws.red, x, r.get(), p.get(), ap.get(), n, sc.get(), s);
   };
   const int64_t c0 = launch_counter();
@@ -619,7 +621,7 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
   readback();
   uint64_t k = 0;
   int64_t graph_launches = 0;
-  double sw_ms = 0.0;
+  double sw_ms = 0.0, op_ms = 0.0;
   while (k < maxit) {
     if (!(hsc->pap > 0.0)) raise(LSAMGDD_ERR_INDEFINITE, "pcg: curvature <p, Ap> is not positive");
     ++k;
@@ -637,6 +639,9 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
     LSB_CUDA(cudaEventElapsedTime(&a, ws.ev[0], ws.ev[1]));
     LSB_CUDA(cudaEventElapsedTime(&b2, ws.ev[2], ws.ev[3]));
     sw_ms += a + b2;
+    float c2 = 0;
+    LSB_CUDA(cudaEventElapsedTime(&c2, ws.ev[4], ws.ev[5]));
+    op_ms += c2;
     if (!(hsc->rz_next > 0.0)) raise(LSAMGDD_ERR_INDEFINITE, "pcg: preconditioned product <r, Br> is not positive");
   }
   out.iterations = k;
@@ -648,6 +653,13 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
     stats->schwarz_ms = sw_ms;
     stats->schwarz_bytes = static_cast<double>(graph_launches) * (h.levels.size() > 1 ? h.levels[0].sm.bytes_ras + h.levels[0].sm.bytes_rast : 0.0);
     stats->schwarz_launches = graph_launches * (h.levels.size() > 1 ? static_cast<int64_t>(h.levels[0].sm.color_off.size()) : 0);
+    // PCG operator y = Gᵀ(G p) (SpMV with G, then with the stored Gᵀ fused with ⟨p, y⟩):
+    // algorithmic bytes B(spmv_G) + B(spmvT_G) of SURVEY.md §8(d)
+    const double nnz = static_cast<double>(g.nnz), mm = static_cast<double>(g.nr), nn = static_cast<double>(n);
+    stats->spmv_ms = op_ms;
+    stats->spmv_bytes = static_cast<double>(graph_launches) *
+                        ((12 * nnz + 4 * (mm + 1) + 8 * nn + 8 * mm) + (12 * nnz + 4 * (nn + 1) + 8 * mm + 8 * nn));
+    stats->spmv_launches = graph_launches * 2;
     stats->total_launches = out.launches;
   }
   return out;

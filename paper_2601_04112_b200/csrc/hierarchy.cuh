@@ -70,7 +70,7 @@ struct SolveWs {
   cudaStream_t s = nullptr;
   std::vector<DBuf<double>> e, res, rhs;  // per level
   Reducer red;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};  // level-0 RAS / RAS-T brackets
+  cudaEvent_t ev[6] = {};  // level-0 RAS / RAS-T brackets, then the PCG operator Gᵀ(G p)
   bool timing = false;
   explicit SolveWs(const Hierarchy& h);
   ~SolveWs();

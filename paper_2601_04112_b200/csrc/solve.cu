@@ -577,6 +577,8 @@ __global__ void __launch_bounds__(kRedThreads) k_ap_dot(const int64_t* __restric
     const int64_t base = soff[i >> 5] + (i & 31);
     const int n = len[i];
     double s = 0.0;
+    // sequential row sum (bit-exact order); the loads of 4 entries are issued ahead
+#pragma unroll 4
     for (int k = 0; k < n; ++k) {
       const int64_t e = base + int64_t(k) * 32;
       s += __ldcs(&val[e]) * __ldg(&gp[__ldcs(&col[e])]);
@@ -674,9 +676,9 @@ void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, c
     schwarz_launch<2>(v, v.order + color_off[c], color_off[c + 1] - color_off[c], r, e, s);
 }
 
-void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s) {
+void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s, bool exact) {
   if (v.n_coarse == 0) return;
-  if (v.n_coarse > 0 && v.n_fine >= 64 * v.n_agg) {  // large aggregates: warp per coarse column
+  if (!exact && v.n_coarse > 0 && v.n_fine >= 64 * v.n_agg) {  // large aggregates: warp per coarse column
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(v.n_coarse, 8), int64_t(sm_count()) * 16)));
     k_restrict_warp<<<grid, 256, 0, s>>>(v, res, rc);
   } else {
@@ -699,7 +701,7 @@ void dense_matvec(const double* m, int64_t n, const double* r, double* e, cudaSt
 }
 
 void Reducer::init(cudaStream_t s) {
-  nblocks = sm_count() * 2;
+  nblocks = sm_count() * 8;  // 8 CTAs of 256 threads per SM: full occupancy for the gather-bound Gᵀ rows
   partial.alloc(nblocks, s);
   ticket.alloc(1, s);
   ticket.zero(s);

@@ -66,7 +66,10 @@ struct InterpView {
 
 // rc = Pᵀ res (spmv_transpose, sparse.hpp:125-137): owner-computes per coarse
 // column, fine rows in ascending order — bit-identical to the scatter.
-void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s);
+// rc = Pᵀ res. `exact`: always the thread-per-column kernel (fine rows
+// ascending, the reference's spmv_transpose order, sparse.hpp:125-137); the
+// V-cycle lets large aggregates use a warp-per-column tree sum instead.
+void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s, bool exact = false);
 // e += P ec (spmv + axpy, hierarchy.hpp:220): per fine row, panel order.
 void prolong_add(const InterpView& v, const double* ec, double* e, cudaStream_t s);
 // e = M r with the explicit coarsest inverse
