@@ -337,6 +337,16 @@ def main() -> None:
                     "kernel": "level-0 Schwarz RAS + RAS-T sweep pair (k_schwarz_lrow: 1 RAS + 4 colour launches)",
                     "bytes_per_launch": ks.schwarz_bytes / max(ks.schwarz_launches, 1),
                     "peak_source": peaks["source"]}
+    # second HBM-bound kernel pair: the PCG operator Gᵀ(G p) (k_sell_spmv + k_ap_dot),
+    # algorithmic bytes B(spmv_G) + B(spmvT_G) of SURVEY.md §8(d)
+    roofline_spmv = None
+    if ks.spmv_ms > 0:
+        a2 = ks.spmv_bytes / (ks.spmv_ms / 1e3) / 1e9
+        roofline_spmv = {"bound": "hbm", "achieved": a2, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": a2 / peaks["hbm_gbs"],
+                         "kernel": "PCG operator y = Gᵀ(G p): k_sell_spmv<0> then k_ap_dot (fused <p, y>)",
+                         "bytes_per_launch": ks.spmv_bytes / max(ks.spmv_launches, 1),
+                         "peak_source": peaks["source"]}
 
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -351,6 +361,7 @@ def main() -> None:
                    "l2": "inputs larger than L2 (G0 CSR %.0f MB > 126 MB)" % (h2d / 1e6),
                    "parallelism": "replicas" if world > 1 else "single"},
         "roofline": roofline,
+        "roofline_spmv": roofline_spmv,
         "e2e": {"value": world * n / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
