@@ -282,10 +282,34 @@ __device__ __forceinline__ double lrow_fixed(const int32_t* __restrict__ ids, co
   return s0 + s1;
 }
 
+// Launch with programmatic stream serialization (PDL): the kernel's
+// griddepcontrol.wait orders it after its predecessor, while its launch and
+// CTA rasterisation overlap the predecessor's drain. LSB_NO_PDL=1 disables
+// the attribute (the waits are then no-ops).
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
+  static const bool pdl = getenv("LSB_NO_PDL") == nullptr;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  LSB_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 template <int MODE>
 __global__ void __launch_bounds__(256) k_schwarz_lrow(SchwarzView v, const int32_t* __restrict__ items, int64_t i0,
                                                       int64_t i1, const double* __restrict__ r,
                                                       double* __restrict__ e) {
+  // Programmatic dependent launch (schwarz_lrow_launch): wait for the
+  // previous kernel's results, then let the next launch start filling the
+  // SMs this grid drains (it waits in turn for this grid to complete).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t it = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < i1; it += warps) {
@@ -368,7 +392,7 @@ void schwarz_lrow_launch(const SchwarzView& v, const int32_t* items, int64_t i0,
                          cudaStream_t s) {
   if (i1 <= i0) return;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * 16)));
-  k_schwarz_lrow<MODE><<<grid, 256, 0, s>>>(v, items, i0, i1, r, e);
+  launch_pdl(k_schwarz_lrow<MODE>, grid, 256, s, v, items, i0, i1, r, e);
   LSB_LAUNCH();
 }
 
@@ -381,6 +405,8 @@ template <int MODE>
 __global__ void __launch_bounds__(256) k_schwarz_rows(SchwarzView v, const int32_t* __restrict__ item_agg,
                                                       const int32_t* __restrict__ item_row, int64_t i0, int64_t i1,
                                                       const double* __restrict__ r, double* __restrict__ e) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL, see k_schwarz_lrow
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
   for (int64_t it = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < i1; it += warps) {
@@ -432,7 +458,7 @@ void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t*
                          const double* r, double* e, cudaStream_t s) {
   if (i1 <= i0) return;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * 8)));
-  k_schwarz_rows<MODE><<<grid, 256, 0, s>>>(v, ia, ir, i0, i1, r, e);
+  launch_pdl(k_schwarz_rows<MODE>, grid, 256, s, v, ia, ir, i0, i1, r, e);
   LSB_LAUNCH();
 }
 
