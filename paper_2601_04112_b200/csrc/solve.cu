@@ -453,12 +453,69 @@ __global__ void __launch_bounds__(256) k_schwarz_rows(SchwarzView v, const int32
   }
 }
 
+// RAS-T rows with L lanes per output row (L < 32 when the level's ω sets are
+// short): 32/L items per warp, so the per-item chain of dependent loads
+// (item -> offsets -> row and ω ids -> r) overlaps across items instead of
+// idling 32 - nω lanes. Sum order: strided lane partial sums, xor tree.
+template <int L>
+__global__ void __launch_bounds__(256) k_schwarz_rows_t(SchwarzView v, const int32_t* __restrict__ item_agg,
+                                                        const int32_t* __restrict__ item_row, int64_t i0, int64_t i1,
+                                                        const double* __restrict__ r, double* __restrict__ e) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL, see k_schwarz_lrow
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  constexpr int PER_WARP = 32 / L;
+  const int lane = threadIdx.x & 31, sub = lane % L;
+  const int64_t teams = int64_t(gridDim.x) * (blockDim.x >> 5) * PER_WARP;
+  const int64_t team0 = (blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5)) * PER_WARP + lane / L;
+  // every lane of a warp runs the same number of iterations (shuffles need the full warp)
+  for (int64_t base = team0 - lane / L; base < i1 - i0; base += teams) {
+    const int64_t it = i0 + base + lane / L;
+    double sum = 0.0;
+    int c = -1;
+    if (it < i1) {
+      const int a = item_agg[it], row = item_row[it];
+      const int32_t* om = v.omega + v.omega_off[a];
+      const int nw = v.omega_off[a + 1] - v.omega_off[a];
+      const int32_t* ga = v.gamma + v.gamma_off[a];
+      const int ng = v.gamma_off[a + 1] - v.gamma_off[a];
+      const double* F = v.row_data + v.row_off[a];
+      const double* fr = row < nw ? F + int64_t(row) * (nw + ng) : F + int64_t(nw) * (nw + ng) + int64_t(row - nw) * nw;
+      double s0 = 0.0, s1 = 0.0;
+      int i = sub;
+      for (; i + L < nw; i += 2 * L) {
+        s0 += __ldcs(&fr[i]) * __ldg(&r[om[i]]);
+        s1 += __ldcs(&fr[i + L]) * __ldg(&r[om[i + L]]);
+      }
+      if (i < nw) s0 += __ldcs(&fr[i]) * __ldg(&r[om[i]]);
+      sum = s0 + s1;
+      if (sub == 0) c = row < nw ? om[row] : ga[row - nw];
+    }
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if (c >= 0) e[c] += sum;
+  }
+}
+
 template <int MODE>
 void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t* ir, int64_t i0, int64_t i1,
                          const double* r, double* e, cudaStream_t s) {
   if (i1 <= i0) return;
   const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * 8)));
-  launch_pdl(k_schwarz_rows<MODE>, grid, 256, s, v, ia, ir, i0, i1, r, e);
+  if (MODE == 2 && v.max_omega <= 64) {
+    // lanes per row: 4 / 8 / 16 for nω up to 8 / 16 / 64 (≤ 4 entries per lane)
+    const int lanes = v.max_omega <= 8 ? 4 : v.max_omega <= 16 ? 8 : 16;
+    const int per_warp = 32 / lanes;
+    const int g2 = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8 * per_warp), int64_t(sm_count()) * 8)));
+    if (lanes == 4)
+      launch_pdl(k_schwarz_rows_t<4>, g2, 256, s, v, ia, ir, i0, i1, r, e);
+    else if (lanes == 8)
+      launch_pdl(k_schwarz_rows_t<8>, g2, 256, s, v, ia, ir, i0, i1, r, e);
+    else
+      launch_pdl(k_schwarz_rows_t<16>, g2, 256, s, v, ia, ir, i0, i1, r, e);
+  } else {
+    launch_pdl(k_schwarz_rows<MODE>, grid, 256, s, v, ia, ir, i0, i1, r, e);
+  }
   LSB_LAUNCH();
 }
 
