@@ -254,7 +254,7 @@ int lsamgdd_level_spmv(const void* handle, int64_t level, int32_t what, int32_t 
           restrict_pt(iv, dx, dy, ws.s, /*exact=*/true);
         } else {
           LSB_CUDA(cudaMemsetAsync(dy, 0, nout * 8, ws.s));
-          prolong_add(iv, dx, dy, ws.s);
+          prolong_add(iv, dx, dy, ws.s, /*exact=*/true);
         }
       });
       return;

@@ -571,6 +571,25 @@ __global__ void k_prolong(InterpView v, const double* __restrict__ ec, double* _
   }
 }
 
+// Wide panels (coarse levels, tens to hundreds of modes per aggregate): warp
+// per fine row, lanes over the row's contiguous panel entries, xor-tree sum.
+__global__ void k_prolong_warp(InterpView v, const double* __restrict__ ec, double* __restrict__ e) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); i < v.n_fine; i += warps) {
+    const int a = v.node_agg[i];
+    const int rr = v.node_pos[i];
+    const int k = v.coarse_off[a + 1] - v.coarse_off[a];
+    const double* row = v.panels + v.panel_off[a] + int64_t(rr) * k;
+    const double* x = ec + v.coarse_off[a];
+    double s = 0.0;
+    for (int j = lane; j < k; j += 32) s += __ldcs(&row[j]) * __ldg(&x[j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) e[i] += s;
+  }
+}
+
 __global__ void k_dense_mv(const double* __restrict__ m, int64_t n, const double* __restrict__ r, double* __restrict__ e) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
@@ -761,7 +780,7 @@ void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, c
 
 void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s, bool exact) {
   if (v.n_coarse == 0) return;
-  if (!exact && v.n_coarse > 0 && v.n_fine >= 64 * v.n_agg) {  // large aggregates: warp per coarse column
+  if (!exact && v.n_coarse > 0 && v.n_fine >= 32 * v.n_agg) {  // large aggregates (mean nω >= 32): warp per coarse column
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(v.n_coarse, 8), int64_t(sm_count()) * 16)));
     k_restrict_warp<<<grid, 256, 0, s>>>(v, res, rc);
   } else {
@@ -770,9 +789,14 @@ void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_
   LSB_LAUNCH();
 }
 
-void prolong_add(const InterpView& v, const double* ec, double* e, cudaStream_t s) {
+void prolong_add(const InterpView& v, const double* ec, double* e, cudaStream_t s, bool exact) {
   if (v.n_fine == 0) return;
-  k_prolong<<<grid_for(v.n_fine), 256, 0, s>>>(v, ec, e);
+  if (!exact && v.n_coarse >= 16 * v.n_agg) {  // ≥ 16 modes per aggregate on average
+    const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(v.n_fine, 8), int64_t(sm_count()) * 8)));
+    k_prolong_warp<<<grid, 256, 0, s>>>(v, ec, e);
+  } else {
+    k_prolong<<<grid_for(v.n_fine), 256, 0, s>>>(v, ec, e);
+  }
   LSB_LAUNCH();
 }
 

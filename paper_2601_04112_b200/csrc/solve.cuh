@@ -70,8 +70,10 @@ struct InterpView {
 // ascending, the reference's spmv_transpose order, sparse.hpp:125-137); the
 // V-cycle lets large aggregates use a warp-per-column tree sum instead.
 void restrict_pt(const InterpView& v, const double* res, double* rc, cudaStream_t s, bool exact = false);
-// e += P ec (spmv + axpy, hierarchy.hpp:220): per fine row, panel order.
-void prolong_add(const InterpView& v, const double* ec, double* e, cudaStream_t s);
+// e += P ec (spmv + axpy, hierarchy.hpp:220): per fine row, panel order
+// (`exact`, the level_spmv export); the V-cycle uses a warp per fine row
+// (tree sum) when the panels are wide.
+void prolong_add(const InterpView& v, const double* ec, double* e, cudaStream_t s, bool exact = false);
 // e = M r with the explicit coarsest inverse
 void dense_matvec(const double* m, int64_t n, const double* r, double* e, cudaStream_t s);
 
