@@ -391,7 +391,15 @@ template <int MODE>
 void schwarz_lrow_launch(const SchwarzView& v, const int32_t* items, int64_t i0, int64_t i1, const double* r, double* e,
                          cudaStream_t s) {
   if (i1 <= i0) return;
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * 16)));
+  // one full wave of resident CTAs (grid-stride over the items): a partial
+  // last wave left most SMs idle during the drain (ncu: 3.2 waves for MODE 2)
+  static const int resident = [] {
+    int b = 0;
+    LSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_schwarz_lrow<MODE>, 256, 0));
+    return std::max(b, 1);
+  }();
+  const int grid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * resident)));
   launch_pdl(k_schwarz_lrow<MODE>, grid, 256, s, v, items, i0, i1, r, e);
   LSB_LAUNCH();
 }
