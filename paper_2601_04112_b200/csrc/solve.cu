@@ -508,13 +508,23 @@ template <int MODE>
 void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t* ir, int64_t i0, int64_t i1,
                          const double* r, double* e, cudaStream_t s) {
   if (i1 <= i0) return;
-  const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * 8)));
+  // grids of one full wave of resident CTAs (see schwarz_lrow_launch)
+  auto resident = [](auto kern) {
+    int b = 0;
+    LSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0));
+    return std::max(b, 1);
+  };
+  static const int res_rows = resident(k_schwarz_rows<MODE>);
+  const int grid = static_cast<int>(
+      std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_rows)));
   if (MODE == 2 && v.max_omega <= 64) {
     // lanes per row: 4 / 8 / 16 for nω up to 8 / 16 / 64 (≤ 4 entries per lane)
     const int lanes = v.max_omega <= 8 ? 4 : v.max_omega <= 16 ? 8 : 16;
     const int per_warp = 32 / lanes;
+    static const int res_t = std::min({resident(k_schwarz_rows_t<4>), resident(k_schwarz_rows_t<8>),
+                                       resident(k_schwarz_rows_t<16>)});
     const int g2 = static_cast<int>(
-        std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8 * per_warp), int64_t(sm_count()) * 8)));
+        std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8 * per_warp), int64_t(sm_count()) * res_t)));
     if (lanes == 4)
       launch_pdl(k_schwarz_rows_t<4>, g2, 256, s, v, ia, ir, i0, i1, r, e);
     else if (lanes == 8)
