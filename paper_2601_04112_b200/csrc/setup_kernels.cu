@@ -760,10 +760,13 @@ void build_row_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, cons
   const int64_t na = topo.n_agg;
   std::vector<int64_t> roff(na + 1, 0);
   std::vector<int32_t> ra, rr, ta, tr;
+  // short rows (nΩ <= 128): a RAS item is a chunk of kRowsCh ω rows sharing
+  // one gather of the Ω ids and r values (k_schwarz_rows_ch)
+  sm.ras_ch = sm.max_sub <= 128 ? kRowsCh : 1;
   for (int64_t i = 0; i < na; ++i) {
     const int64_t nw = hoo[i + 1] - hoo[i], ng = hgo[i + 1] - hgo[i];
     roff[i + 1] = roff[i] + nw * (nw + ng) + ng * nw;
-    for (int64_t r = 0; r < nw; ++r) {
+    for (int64_t r = 0; r < nw; r += sm.ras_ch) {
       ra.push_back(static_cast<int32_t>(i));
       rr.push_back(static_cast<int32_t>(r));
     }

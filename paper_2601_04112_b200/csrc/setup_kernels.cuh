@@ -57,12 +57,14 @@ struct DevSmoother {
   bool rows = false;
   DBuf<int64_t> row_off;              // n_agg + 1 (doubles)
   DBuf<double> row_data;
-  DBuf<int32_t> ras_agg, ras_row;     // RAS work items: (aggregate, ω row)
+  DBuf<int32_t> ras_agg, ras_row;     // RAS work items: (aggregate, first ω row of a chunk of ras_ch rows)
+  int ras_ch = 1;
   DBuf<int32_t> rast_agg, rast_row;   // RAS-T work items, colour-sorted: (aggregate, Ω row)
   std::vector<int64_t> rast_color_off;  // host, n_colors + 1
 };
 
 constexpr int kLaneMaxSub = 48;
+constexpr int kRowsCh = 4;  // ω rows per RAS item in the row layout when nΩ <= 128
 constexpr int64_t kRowsMinBlk = 0;  // larger blocks use the row layout (warp per output row)
 constexpr int kLaneMaxOmega = 24;
 

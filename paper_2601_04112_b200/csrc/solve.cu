@@ -504,6 +504,58 @@ __global__ void __launch_bounds__(256) k_schwarz_rows_t(SchwarzView v, const int
   }
 }
 
+// RAS on short rows (nΩ <= 128): one warp per chunk of kRowsCh consecutive
+// ω rows of one aggregate; the lane's Ω ids and r values (j = lane + 32t) are
+// gathered once per chunk, then each row is the same even/odd-split lane sum
+// and xor tree as k_schwarz_rows, so the results are bit-identical to it.
+template <int MODE>
+__global__ void __launch_bounds__(256) k_schwarz_rows_ch(SchwarzView v, const int32_t* __restrict__ item_agg,
+                                                         const int32_t* __restrict__ item_row, int64_t i0, int64_t i1,
+                                                         const double* __restrict__ r, double* __restrict__ e) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL, see k_schwarz_lrow
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t it = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < i1; it += warps) {
+    const int a = item_agg[it], row0 = item_row[it];
+    const int32_t* om = v.omega + v.omega_off[a];
+    const int nw = v.omega_off[a + 1] - v.omega_off[a];
+    const int32_t* ga = v.gamma + v.gamma_off[a];
+    const int ng = v.gamma_off[a + 1] - v.gamma_off[a];
+    const int m = nw + ng;
+    const double* F = v.row_data + v.row_off[a];
+    double rv[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int j = lane + 32 * t;
+      rv[t] = j < m ? __ldg(&r[j < nw ? om[j] : ga[j - nw]]) : 0.0;
+    }
+    const int rend = row0 + kRowsCh < nw ? row0 + kRowsCh : nw;
+    for (int row = row0; row < rend; ++row) {
+      const double* fr = F + int64_t(row) * m;
+      double f[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) f[t] = lane + 32 * t < m ? __ldcs(&fr[lane + 32 * t]) : 0.0;
+      // k_schwarz_rows' order: s0 over t = 0, 2 and s1 over t = 1, 3, each
+      // term only where its column exists
+      double s0 = 0.0, s1 = 0.0;
+      if (lane < m) s0 += f[0] * rv[0];
+      if (lane + 32 < m) s1 += f[1] * rv[1];
+      if (lane + 64 < m) s0 += f[2] * rv[2];
+      if (lane + 96 < m) s1 += f[3] * rv[3];
+      double sum = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) {
+        if (MODE == 0)
+          e[om[row]] = sum;
+        else
+          e[om[row]] += sum;
+      }
+    }
+  }
+}
+
 template <int MODE>
 void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t* ir, int64_t i0, int64_t i1,
                          const double* r, double* e, cudaStream_t s) {
@@ -517,7 +569,12 @@ void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t*
   static const int res_rows = resident(k_schwarz_rows<MODE>);
   const int grid = static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_rows)));
-  if (MODE == 2 && v.max_omega <= 64) {
+  if (MODE < 2 && v.ras_ch > 1) {
+    static const int res_ch = resident(k_schwarz_rows_ch<MODE>);
+    const int g3 = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_ch)));
+    launch_pdl(k_schwarz_rows_ch<MODE>, g3, 256, s, v, ia, ir, i0, i1, r, e);
+  } else if (MODE == 2 && v.max_omega <= 64) {
     // lanes per row: 4 / 8 / 16 for nω up to 8 / 16 / 64 (≤ 4 entries per lane)
     const int lanes = v.max_omega <= 8 ? 4 : v.max_omega <= 16 ? 8 : 16;
     const int per_warp = 32 / lanes;
