@@ -318,6 +318,7 @@ SchwarzView Level::schwarz_view() const {
   v.ras_row = sm.ras_row.get();
   v.n_ras_items = static_cast<int64_t>(sm.ras_agg.size());
   v.ras_ch = sm.ras_ch;
+  v.rast_ch = sm.rast_ch;
   v.rast_agg = sm.rast_agg.get();
   v.rast_row = sm.rast_row.get();
   v.rast_color_off = &sm.rast_color_off;

@@ -772,11 +772,15 @@ void build_row_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, cons
     }
   }
   sm.rast_color_off.assign(sm.color_off.size(), 0);
+  // 64 < nω <= 128: a RAS-T item is a chunk of kRowsCh Ω rows sharing one
+  // gather of the ω ids and r values (k_schwarz_rows_tch); shorter ω sets
+  // take the sub-warp rows of k_schwarz_rows_t instead
+  sm.rast_ch = sm.max_omega > 64 && sm.max_omega <= 128 ? kRowsCh : 1;
   for (size_t c = 0; c + 1 < sm.color_off.size(); ++c) {
     for (int64_t k = sm.color_off[c]; k < sm.color_off[c + 1]; ++k) {
       const int32_t a = byc[k];
       const int64_t m = (hoo[a + 1] - hoo[a]) + (hgo[a + 1] - hgo[a]);
-      for (int64_t r = 0; r < m; ++r) {
+      for (int64_t r = 0; r < m; r += sm.rast_ch) {
         ta.push_back(a);
         tr.push_back(static_cast<int32_t>(r));
       }

@@ -59,6 +59,7 @@ struct DevSmoother {
   DBuf<double> row_data;
   DBuf<int32_t> ras_agg, ras_row;     // RAS work items: (aggregate, first ω row of a chunk of ras_ch rows)
   int ras_ch = 1;
+  int rast_ch = 1;                    // Ω rows per RAS-T item
   DBuf<int32_t> rast_agg, rast_row;   // RAS-T work items, colour-sorted: (aggregate, Ω row)
   std::vector<int64_t> rast_color_off;  // host, n_colors + 1
 };

@@ -556,6 +556,50 @@ __global__ void __launch_bounds__(256) k_schwarz_rows_ch(SchwarzView v, const in
   }
 }
 
+// RAS-T counterpart of k_schwarz_rows_ch (nω <= 128): chunks of kRowsCh Ω
+// rows share one gather of the ω ids and r values; per row the sum order of
+// k_schwarz_rows<2> (bit-identical).
+__global__ void __launch_bounds__(256) k_schwarz_rows_tch(SchwarzView v, const int32_t* __restrict__ item_agg,
+                                                          const int32_t* __restrict__ item_row, int64_t i0,
+                                                          int64_t i1, const double* __restrict__ r,
+                                                          double* __restrict__ e) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL, see k_schwarz_lrow
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t it = i0 + blockIdx.x * int64_t(blockDim.x >> 5) + (threadIdx.x >> 5); it < i1; it += warps) {
+    const int a = item_agg[it], row0 = item_row[it];
+    const int32_t* om = v.omega + v.omega_off[a];
+    const int nw = v.omega_off[a + 1] - v.omega_off[a];
+    const int32_t* ga = v.gamma + v.gamma_off[a];
+    const int ng = v.gamma_off[a + 1] - v.gamma_off[a];
+    const int m = nw + ng;
+    const double* F = v.row_data + v.row_off[a];
+    double rv[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const int i = lane + 32 * t;
+      rv[t] = i < nw ? __ldg(&r[om[i]]) : 0.0;
+    }
+    const int rend = row0 + kRowsCh < m ? row0 + kRowsCh : m;
+    for (int row = row0; row < rend; ++row) {
+      const double* fr = row < nw ? F + int64_t(row) * m : F + int64_t(nw) * m + int64_t(row - nw) * nw;
+      double f[4];
+#pragma unroll
+      for (int t = 0; t < 4; ++t) f[t] = lane + 32 * t < nw ? __ldcs(&fr[lane + 32 * t]) : 0.0;
+      double s0 = 0.0, s1 = 0.0;
+      if (lane < nw) s0 += f[0] * rv[0];
+      if (lane + 32 < nw) s1 += f[1] * rv[1];
+      if (lane + 64 < nw) s0 += f[2] * rv[2];
+      if (lane + 96 < nw) s1 += f[3] * rv[3];
+      double sum = s0 + s1;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+      if (lane == 0) e[row < nw ? om[row] : ga[row - nw]] += sum;
+    }
+  }
+}
+
 template <int MODE>
 void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t* ir, int64_t i0, int64_t i1,
                          const double* r, double* e, cudaStream_t s) {
@@ -574,6 +618,11 @@ void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t*
     const int g3 = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_ch)));
     launch_pdl(k_schwarz_rows_ch<MODE>, g3, 256, s, v, ia, ir, i0, i1, r, e);
+  } else if (MODE == 2 && v.rast_ch > 1) {
+    static const int res_tch = resident(k_schwarz_rows_tch);
+    const int g3 = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_tch)));
+    launch_pdl(k_schwarz_rows_tch, g3, 256, s, v, ia, ir, i0, i1, r, e);
   } else if (MODE == 2 && v.max_omega <= 64) {
     // lanes per row: 4 / 8 / 16 for nω up to 8 / 16 / 64 (≤ 4 entries per lane)
     const int lanes = v.max_omega <= 8 ? 4 : v.max_omega <= 16 ? 8 : 16;

@@ -38,7 +38,8 @@ struct SchwarzView {
   const int32_t* ras_agg;
   const int32_t* ras_row;
   int64_t n_ras_items;
-  int ras_ch;  // ω rows per RAS item (DevSmoother::ras_ch)
+  int ras_ch;   // ω rows per RAS item (DevSmoother::ras_ch)
+  int rast_ch;  // Ω rows per RAS-T item (DevSmoother::rast_ch)
   const int32_t* rast_agg;
   const int32_t* rast_row;
   const std::vector<int64_t>* rast_color_off;
