@@ -16,6 +16,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "jacobi_wave.cuh"
 
 namespace lsb {
 
@@ -26,6 +27,10 @@ struct Arena {
   int64_t used;
   double* fast = nullptr;   // optional shared-memory scratch (CTA teams, global workspace)
   int64_t fast_cap = 0;     // doubles
+  WaveCtl* wctl = nullptr;  // cluster launches: command block and workspace of the wavefront Jacobi
+  double* wws = nullptr;
+  int wave_min = 0;         // smallest n that takes the wavefront path
+  int sched = 0;            // schedule of the single-CTA large-n path (test hook)
   __device__ double* take(int64_t n) {
     double* p = base + used;
     used += (n + 1) & ~int64_t(1);
@@ -679,22 +684,14 @@ __device__ int cta_sym_eig_pc(int n, const double* m, double* vals, double* vecs
   return 0;
 }
 
-#include "jacobi2.cuh"
-
-__device__ int g_eig_split = 3;
-  // 1: producer/consumer, 0: one barrier per rotation (test hook)
-
+// sched 0: producer/consumer with 15 consumer warps (default); 1: one barrier
+// per rotation (the only schedule for n > 384*kMaxOwn; also a test path)
 __device__ __noinline__ int cta_sym_eig_pipelined_any(int n, const double* m, double* vals, double* vecs, double* A,
-                                                double* Vt, double* sm, int R) {
-  if (g_eig_split == 3 && n <= 384 * kMaxOwn) {
+                                                double* Vt, double* sm, int R, int sched) {
+  if (sched == 0 && n <= 384 * kMaxOwn) {
     if (R >= 8) return cta_sym_eig_pc<8, 15>(n, m, vals, vecs, A, Vt, sm);
     if (R >= 6) return cta_sym_eig_pc<6, 15>(n, m, vals, vecs, A, Vt, sm);
     return cta_sym_eig_pc<4, 15>(n, m, vals, vecs, A, Vt, sm);
-  }
-  if (g_eig_split && n <= 384 * kMaxOwn) {
-    if (R >= 8) return cta_sym_eig_pc<8>(n, m, vals, vecs, A, Vt, sm);
-    if (R >= 6) return cta_sym_eig_pc<6>(n, m, vals, vecs, A, Vt, sm);
-    return cta_sym_eig_pc<4>(n, m, vals, vecs, A, Vt, sm);
   }
   if (R >= 8) return cta_sym_eig_pipelined<8>(n, m, vals, vecs, A, Vt, sm);
   if (R >= 6) return cta_sym_eig_pipelined<6>(n, m, vals, vecs, A, Vt, sm);
@@ -787,21 +784,8 @@ __device__ int t_sym_eig(const Team& t, int n, const double* m, double* vals, do
     return 0;
   }
   if constexpr (!std::is_same<Team, WarpTeam>::value) {
-    if (ar.fast && n >= 48 && blockDim.x == kPipeThreads && g_eig_split == 2 && n <= 768) {
-      int RA = 12, NO = 22;
-      while (jac2_smem_doubles(n, RA, NO) > ar.fast_cap && RA > 8) {
-        RA -= 1;
-        NO -= 1;
-      }
-      if (jac2_smem_doubles(n, RA, NO) <= ar.fast_cap) {
-        const int64_t ld4 = jac2_ld(n);
-        double* A = ar.take(int64_t(n) * ld4);
-        double* Vt = ar.take(int64_t(n) * ld4);
-        if (n <= 256) return cta_sym_eig_jac2<8>(n, m, vals, vecs, A, Vt, ar.fast, RA, NO);
-        if (n <= 512) return cta_sym_eig_jac2<16>(n, m, vals, vecs, A, Vt, ar.fast, RA, NO);
-        return cta_sym_eig_jac2<24>(n, m, vals, vecs, A, Vt, ar.fast, RA, NO);
-      }
-    }
+    if (ar.wctl && n >= ar.wave_min && n <= kWaveMaxN && wave_smem_doubles(n) <= ar.fast_cap)
+      return wave_sym_eig_leader(n, m, vals, vecs, ar.wctl, ar.wws, ar.fast);
     if (ar.fast && n >= 48 && blockDim.x == kPipeThreads) {
       int R = 8;
       while (R > 4 && pipelined_smem_doubles(n, R) > ar.fast_cap) R -= 2;
@@ -809,7 +793,7 @@ __device__ int t_sym_eig(const Team& t, int n, const double* m, double* vals, do
         const int64_t ld = (n + 1) & ~int64_t(1);
         double* A = ar.take(int64_t(n) * ld);
         double* Vt = ar.take(int64_t(n) * ld);
-        return cta_sym_eig_pipelined_any(n, m, vals, vecs, A, Vt, ar.fast, R);
+        return cta_sym_eig_pipelined_any(n, m, vals, vecs, A, Vt, ar.fast, R, ar.sched);
       }
     }
   }

@@ -160,7 +160,7 @@ __device__ long long* g_gevp_prof = nullptr;
 
 template <class Team>
 __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* ws, double* fast = nullptr,
-                             int64_t fast_cap = 0) {
+                             int64_t fast_cap = 0, WaveCtl* wctl = nullptr, double* wws = nullptr, int wave_min = 0) {
   const int agg = g.list[idx];
   long long* const gprof = g_gevp_prof;
   long long ck = gprof ? clock64() : 0;
@@ -177,6 +177,9 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
   const int ng = g.gamma_off[agg + 1] - g.gamma_off[agg];
   constexpr double tau_rel = 1e-10;
   Arena ar{ws, 0, fast, fast_cap};
+  ar.wctl = wctl;
+  ar.wws = wws;
+  ar.wave_min = wave_min;
   double* slot = ar.take(8);
   double* L = ar.take(int64_t(nw) * nw);
   double* W = ar.take(int64_t(nw) * nw);
@@ -379,6 +382,9 @@ __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
 // shared doubles for the pipelined Jacobi: 207 KiB dynamic + the kernels'
 // static shared arrays (15 KiB) stay within the 227 KiB per CTA
 constexpr int64_t kFastCap = 26500;
+constexpr int kWaveCluster = 4;  // CTAs per cluster of the wavefront Jacobi: 1 leader + 3 replay CTAs
+constexpr int64_t kWaveClassMin = 160;  // subdomains with max(nω, nΓ) >= this run in clusters
+constexpr int kWaveMinN = 96;           // ... and their eigensolves with n >= this take the wavefront path
 
 template <bool SMEM>
 __global__ void __launch_bounds__(512) k_gevp_block(GevpArgs g) {
@@ -390,6 +396,27 @@ __global__ void __launch_bounds__(512) k_gevp_block(GevpArgs g) {
     else
       gevp_problem(t, g, idx, ws, dyn_smem, kFastCap);
   }
+}
+
+// Large subdomains: one cluster per problem slot. CTA 0 runs the problem; its
+// eigensolves with n >= wave_min take the wavefront Jacobi (jacobi_wave.cuh),
+// for which CTAs 1..C-1 replay the rotation log on V and the finished rows.
+constexpr int64_t kWaveSmemCap = 27800;  // doubles: wave_smem_doubles(608)
+__global__ void __launch_bounds__(512, 1) k_gevp_wave(GevpArgs g, WaveCtl* ctls, double* wws, int64_t wws_stride,
+                                                    int wave_min) {
+  const cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
+  const int C = static_cast<int>(cl.num_blocks());
+  const int slot = blockIdx.x / C, nslots = gridDim.x / C;
+  WaveCtl* ctl = ctls + slot;
+  if (cl.block_rank() != 0) {
+    wave_helper_main(ctl);
+    return;
+  }
+  BlockTeam t;
+  double* ws = g.gws + int64_t(slot) * g.ws_stride;
+  for (int idx = slot; idx < g.n_list; idx += nslots)
+    gevp_problem(t, g, idx, ws, dyn_smem, kWaveSmemCap, ctl, wws + int64_t(slot) * wws_stride, wave_min);
+  wave_quit(ctl);
 }
 
 // ---- smoother blocks (smoother.hpp:38-58, dense.hpp:119-185) ---------------------
@@ -924,56 +951,74 @@ __global__ void k_dense_eig_warp(int n, const double* a, double* vals, double* v
 }
 
 __global__ void __launch_bounds__(512) k_dense_eig_block(int n, const double* a, double* vals, double* vecs, double* ws, int32_t* status,
-                                  int use_fast) {
+                                  int use_fast, int sched) {
   BlockTeam t;
   Arena ar{ws, 0, use_fast ? dyn_smem : nullptr, use_fast ? kFastCap : 0};
+  ar.sched = sched;
   const int st = t_sym_eig(t, n, a, vals, vecs, ar);
   if (t.rank() == 0) *status = st;
 }
 
+// one cluster: CTA 0 runs the wavefront Jacobi, the other CTAs replay its rotation log
+__global__ void __launch_bounds__(512, 1) k_dense_eig_wave(int n, const double* a, double* vals, double* vecs, double* ws,
+                                                        WaveCtl* ctl, int32_t* status) {
+  if (cooperative_groups::this_cluster().block_rank() != 0) {
+    wave_helper_main(ctl);
+    return;
+  }
+  const int st = wave_sym_eig_leader(n, a, vals, vecs, ctl, ws, dyn_smem);
+  if (threadIdx.x == 0) *status = st;
+  wave_quit(ctl);
+}
+
 }  // namespace
 
+// Test hook: one eigensolve on a chosen device path. 0: warp team, 1: CTA
+// team, 2: CTA producer/consumer pipeline, 3: CTA pipeline with one barrier
+// per rotation, 4: cluster wavefront (jacobi_wave.cuh).
 int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, int path, cudaStream_t s) {
-  {
-    // 3: p/c with 15 consumer warps (default), 1: p/c with 12, 2: row-p warps (experimental), 0: pipelined
-    const char* e = getenv("LSB_EIG_SPLIT");
-    const int split = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
-    LSB_CUDA(cudaMemcpyToSymbol(g_eig_split, &split, sizeof(split)));
-    const char* dv = getenv("LSB_JAC2_DBG");
-    const int dbg = dv ? (dv[0] == '2' ? 2 : 1) : 0;
-    LSB_CUDA(cudaMemcpyToSymbol(g_jac2_dbg, &dbg, sizeof(dbg)));
-  }
-  if (getenv("LSB_EIG_PROF")) {
-    static long long* buf = nullptr;
-    if (!buf) LSB_CUDA(cudaMalloc(&buf, 8 * sizeof(long long)));
-    LSB_CUDA(cudaMemset(buf, 0, 8 * sizeof(long long)));
-    LSB_CUDA(cudaMemcpyToSymbol(g_eig_prof, &buf, sizeof(buf)));
-  }
+  if (path == 4 && (n < 2 || n > kWaveMaxN)) raise(LSAMGDD_ERR_INPUT, "dense_sym_eig: wavefront path needs 2 <= n <= 608");
   DBuf<double> a(n * n, s), vals(std::max<int64_t>(n, 1), s), vecs(std::max<int64_t>(n * n, 1), s),
-      ws(sym_eig_scratch(n) + 64, s);
+      ws((path == 4 ? wave_ws_doubles(n) : sym_eig_scratch(n)) + 64, s);
   DBuf<int32_t> st(1, s);
   st.zero(s);
   a.upload(h_a, n * n, s);
   if (path == 0) {
     k_dense_eig_warp<<<1, 32, 0, s>>>(static_cast<int>(n), a.get(), vals.get(), vecs.get(), ws.get(), st.get());
+  } else if (path == 4) {
+    DBuf<WaveCtl> ctl(1, s);
+    ctl.zero(s);
+    const size_t smem = size_t(wave_smem_doubles(n)) * 8;
+    LSB_CUDA(cudaFuncSetAttribute(k_dense_eig_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(kWaveCluster);
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = kWaveCluster;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    LSB_CUDA(cudaLaunchKernelEx(&cfg, k_dense_eig_wave, static_cast<int>(n), static_cast<const double*>(a.get()),
+                                vals.get(), vecs.get(), ws.get(), ctl.get(), st.get()));
+    LSB_LAUNCH();
+    const int status = read_scalar(st.get(), s);
+    const auto hv = vals.download(s);
+    const auto hV = vecs.download(s);
+    std::copy(hv.begin(), hv.begin() + n, h_vals);
+    std::copy(hV.begin(), hV.begin() + n * n, h_vecs);
+    return status;
   } else {
-    const size_t fsm = path == 2 ? size_t(kFastCap) * 8 : 0;
+    const size_t fsm = path >= 2 ? size_t(kFastCap) * 8 : 0;
     LSB_CUDA(cudaFuncSetAttribute(k_dense_eig_block, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kFastCap * 8)));
     k_dense_eig_block<<<1, 512, fsm, s>>>(static_cast<int>(n), a.get(), vals.get(), vecs.get(), ws.get(), st.get(),
-                                          path == 2 ? 1 : 0);
+                                          path >= 2 ? 1 : 0, path == 3 ? 1 : 0);
   }
   LSB_LAUNCH();
   const int status = read_scalar(st.get(), s);
-  if (getenv("LSB_EIG_PROF")) {
-    long long* dp = nullptr;
-    LSB_CUDA(cudaMemcpyFromSymbol(&dp, g_eig_prof, sizeof(dp)));
-    if (dp) {
-      long long h[8];
-      LSB_CUDA(cudaMemcpy(h, dp, sizeof(h), cudaMemcpyDeviceToHost));
-      fprintf(stderr, "eig prof (Mcycles): %.1f %.1f %.1f %.1f %.1f %.1f steps %lld rounds %lld\n",
-              h[0] / 1e6, h[1] / 1e6, h[2] / 1e6, h[3] / 1e6, h[4] / 1e6, h[5] / 1e6, h[6], h[7]);
-    }
-  }
   const auto hv = vals.download(s);
   const auto hV = vecs.download(s);
   std::copy(hv.begin(), hv.begin() + n, h_vals);
@@ -1119,10 +1164,6 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_check, &chk, sizeof(chk), 0, cudaMemcpyHostToDevice, s));
     LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_bad, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
   }
-  if (const char* e = getenv("LSB_EIG_SPLIT")) {  // Jacobi schedule override (experiments)
-    const int split = (e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
-    LSB_CUDA(cudaMemcpyToSymbolAsync(g_eig_split, &split, sizeof(split), 0, cudaMemcpyHostToDevice, s));
-  }
   const bool prof_on = getenv("LSB_GEVP_PROF") != nullptr;
   DBuf<long long> eprof(prof_on ? 8 : 1, s);
   if (prof_on) {
@@ -1189,14 +1230,22 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
   std::vector<DBuf<int32_t>> chunk_list(chunks.size());
   for (size_t ci = 0; ci < chunks.size(); ++ci) {
     const int64_t a0 = chunks[ci].first, a1 = chunks[ci].second;
-    std::vector<int32_t> aggs;
-    for (int64_t a = a0; a < a1; ++a) aggs.push_back(static_cast<int32_t>(a));
+    // subdomains whose eigenproblems are large enough for the cluster wavefront Jacobi
+    auto wave_class = [&](int64_t a) {
+      const int64_t nw = hoo[a + 1] - hoo[a], ng = hgo[a + 1] - hgo[a], mx = std::max(nw, ng);
+      return mx >= kWaveClassMin && mx <= kWaveMaxN;
+    };
+    std::vector<int32_t> aggs, big;
+    for (int64_t a = a0; a < a1; ++a) (wave_class(a) ? big : aggs).push_back(static_cast<int32_t>(a));
     // classes decide the list order; panel scratch offsets follow that order
     std::vector<int32_t> order;
     {
       std::vector<int32_t> cls[3];
       for (int32_t a : aggs) cls[ws_class(need[a])].push_back(a);
       for (int c = 0; c < 3; ++c) order.insert(order.end(), cls[c].begin(), cls[c].end());
+      // largest first: the longest problems start first
+      std::stable_sort(big.begin(), big.end(), [&](int32_t x, int32_t y) { return need[x] > need[y]; });
+      order.insert(order.end(), big.begin(), big.end());
     }
     std::vector<int64_t> toff(order.size() + 1, 0);
     for (size_t k = 0; k < order.size(); ++k) {
@@ -1228,7 +1277,49 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     g.pre = pre.get();
     g.pre_off = pre.get() ? pre_off.get() : nullptr;
     std::vector<int32_t> lo;
-    launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, s);
+    if (!aggs.empty()) launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, s);
+    DBuf<int32_t> big_list;
+    if (!big.empty()) {
+      const int base = static_cast<int>(lo.size());
+      const int cnt = static_cast<int>(big.size());
+      int64_t wmax = 0, nmax = 0;
+      for (int32_t a : big) {
+        wmax = std::max(wmax, need[a]);
+        nmax = std::max<int64_t>(nmax, std::max(hoo[a + 1] - hoo[a], hgo[a + 1] - hgo[a]));
+      }
+      wmax = r2(wmax);
+      const int64_t wws = r2(wave_ws_doubles(nmax));
+      // one cluster per slot; bound the footprint to ~2 GiB
+      const int64_t slots = std::max<int64_t>(1, std::min<int64_t>({int64_t(cnt), int64_t(sm_count()) / kWaveCluster,
+                                                                    (int64_t(1) << 28) / std::max<int64_t>(wmax + wws, 1)}));
+      big_list.upload(big, s);
+      DBuf<double> gws(slots * wmax, s), wbuf(slots * wws, s);
+      DBuf<WaveCtl> ctls(slots, s);
+      ctls.zero(s);
+      GevpArgs gb = g;
+      gb.list = big_list.get();
+      gb.list_base = base;
+      gb.n_list = cnt;
+      gb.ws_stride = wmax;
+      gb.gws = gws.get();
+      const size_t smem = size_t(kWaveSmemCap) * 8;
+      LSB_CUDA(cudaFuncSetAttribute(k_gevp_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(slots * kWaveCluster));
+      cfg.blockDim = dim3(512);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kWaveCluster;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      LSB_CUDA(cudaLaunchKernelEx(&cfg, k_gevp_wave, gb, ctls.get(), wbuf.get(), wws, static_cast<int>(kWaveMinN)));
+      LSB_LAUNCH();
+      lo.insert(lo.end(), big.begin(), big.end());
+    }
     chunk_list[ci].upload(lo, s);
   }
   if (prof_on) {
