@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(512, 1) k_gevp_wave(GevpArgs g, WaveCtl* ctls,
   const int slot = blockIdx.x / C, nslots = gridDim.x / C;
   WaveCtl* ctl = ctls + slot;
   if (cl.block_rank() != 0) {
-    wave_helper_main(ctl);
+    wave_helper_main(ctl, dyn_smem);
     return;
   }
   BlockTeam t;
@@ -963,7 +963,7 @@ __global__ void __launch_bounds__(512) k_dense_eig_block(int n, const double* a,
 __global__ void __launch_bounds__(512, 1) k_dense_eig_wave(int n, const double* a, double* vals, double* vecs, double* ws,
                                                         WaveCtl* ctl, int32_t* status) {
   if (cooperative_groups::this_cluster().block_rank() != 0) {
-    wave_helper_main(ctl);
+    wave_helper_main(ctl, dyn_smem);
     return;
   }
   const int st = wave_sym_eig_leader(n, a, vals, vecs, ctl, ws, dyn_smem);
@@ -988,6 +988,14 @@ int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, 
   } else if (path == 4) {
     DBuf<WaveCtl> ctl(1, s);
     ctl.zero(s);
+    DBuf<long long> prof(16, s);
+    prof.zero(s);
+    const bool want_prof = getenv("LSB_WAVE_PROF") != nullptr;  // diagnostic: phase cycle counters of this test hook
+    if (want_prof) {
+      long long* pp = prof.get();
+      LSB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctl.get()) + offsetof(WaveCtl, prof), &pp, sizeof(pp),
+                               cudaMemcpyHostToDevice, s));
+    }
     const size_t smem = size_t(wave_smem_doubles(n)) * 8;
     LSB_CUDA(cudaFuncSetAttribute(k_dense_eig_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     cudaLaunchConfig_t cfg = {};
@@ -1006,6 +1014,13 @@ int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, 
                                 vals.get(), vecs.get(), ws.get(), ctl.get(), st.get()));
     LSB_LAUNCH();
     const int status = read_scalar(st.get(), s);
+    if (want_prof) {
+      const auto hp = prof.download(s);
+      fprintf(stderr, "wave prof n=%lld (Mcycles): warps: wait %.1f first %.1f pivots %.1f second %.1f finalise %.1f | "
+              "diag-load %.1f diag-writeback %.1f steps %lld | leader: init %.1f sum %.1f wavefront %.1f helper-wait %.1f copyback %.1f | sweeps %lld rotations %lld\n", (long long)n,
+              hp[0] / 1e6, hp[1] / 1e6, hp[2] / 1e6, hp[3] / 1e6, hp[4] / 1e6, hp[12] / 1e6, hp[13] / 1e6, hp[14], hp[10] / 1e6, hp[5] / 1e6, hp[11] / 1e6, hp[6] / 1e6,
+              hp[7] / 1e6, hp[8], hp[9]);
+    }
     const auto hv = vals.download(s);
     const auto hV = vecs.download(s);
     std::copy(hv.begin(), hv.begin() + n, h_vals);
