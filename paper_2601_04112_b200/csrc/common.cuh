@@ -129,6 +129,10 @@ struct BlockTeam {
   __device__ int size() const { return blockDim.x; }
   __device__ void sync() const { __syncthreads(); }
 };
+// The leader CTA of a cluster launch: a BlockTeam whose eigensolves all take
+// the cluster wavefront path (no single-CTA pipeline, whose static shared
+// arrays would not fit beside the wavefront's staging buffers).
+struct ClusterLeadTeam : BlockTeam {};
 #endif
 
 }  // namespace lsb

@@ -786,7 +786,7 @@ __device__ int t_sym_eig(const Team& t, int n, const double* m, double* vals, do
   if constexpr (!std::is_same<Team, WarpTeam>::value) {
     if (ar.wctl && n >= ar.wave_min && n <= kWaveMaxN && wave_smem_doubles(n) <= ar.fast_cap)
       return wave_sym_eig_leader(n, m, vals, vecs, ar.wctl, ar.wws, ar.fast);
-    if (ar.fast && n >= 48 && blockDim.x == kPipeThreads) {
+    if (std::is_same<Team, BlockTeam>::value && ar.fast && n >= 48 && blockDim.x == kPipeThreads) {
       int R = 8;
       while (R > 4 && pipelined_smem_doubles(n, R) > ar.fast_cap) R -= 2;
       if (pipelined_smem_doubles(n, R) <= ar.fast_cap) {

@@ -369,7 +369,7 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
   mark(4);
 }
 
-extern __shared__ double dyn_smem[];
+extern __shared__ __align__(128) double dyn_smem[];
 
 template <int WPB>
 __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
@@ -383,8 +383,9 @@ __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
 // static shared arrays (15 KiB) stay within the 227 KiB per CTA
 constexpr int64_t kFastCap = 26500;
 constexpr int kWaveCluster = 4;  // CTAs per cluster of the wavefront Jacobi: 1 leader + 3 replay CTAs
-constexpr int64_t kWaveClassMin = 160;  // subdomains with max(nω, nΓ) >= this run in clusters
-constexpr int kWaveMinN = 96;           // ... and their eigensolves with n >= this take the wavefront path
+constexpr int64_t kWaveClassMin = 128;  // subdomains with max(nω, nΓ) >= this run in clusters
+constexpr int64_t kWaveSmallMax = 256;  // ... of 2 CTAs up to this size, of 4 CTAs above
+constexpr int kWaveMinN = 1;            // ... where every eigensolve takes the wavefront path
 
 template <bool SMEM>
 __global__ void __launch_bounds__(512) k_gevp_block(GevpArgs g) {
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(512) k_gevp_block(GevpArgs g) {
 // Large subdomains: one cluster per problem slot. CTA 0 runs the problem; its
 // eigensolves with n >= wave_min take the wavefront Jacobi (jacobi_wave.cuh),
 // for which CTAs 1..C-1 replay the rotation log on V and the finished rows.
-constexpr int64_t kWaveSmemCap = 27800;  // doubles: wave_smem_doubles(608)
+constexpr int64_t kWaveSmemCap = 28752;  // doubles: wave_smem_doubles(608)
 __global__ void __launch_bounds__(512, 1) k_gevp_wave(GevpArgs g, WaveCtl* ctls, double* wws, int64_t wws_stride,
                                                     int wave_min) {
   const cooperative_groups::cluster_group cl = cooperative_groups::this_cluster();
@@ -412,7 +413,7 @@ __global__ void __launch_bounds__(512, 1) k_gevp_wave(GevpArgs g, WaveCtl* ctls,
     wave_helper_main(ctl, dyn_smem);
     return;
   }
-  BlockTeam t;
+  ClusterLeadTeam t;
   double* ws = g.gws + int64_t(slot) * g.ws_stride;
   for (int idx = slot; idx < g.n_list; idx += nslots)
     gevp_problem(t, g, idx, ws, dyn_smem, kWaveSmemCap, ctl, wws + int64_t(slot) * wws_stride, wave_min);
@@ -1258,9 +1259,13 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
       std::vector<int32_t> cls[3];
       for (int32_t a : aggs) cls[ws_class(need[a])].push_back(a);
       for (int c = 0; c < 3; ++c) order.insert(order.end(), cls[c].begin(), cls[c].end());
-      // largest first: the longest problems start first
+      // largest first: the longest problems start first (the > 256 class launches before the <= 256 class)
       std::stable_sort(big.begin(), big.end(), [&](int32_t x, int32_t y) { return need[x] > need[y]; });
-      order.insert(order.end(), big.begin(), big.end());
+      auto big_mx = [&](int32_t a) { return std::max(hoo[a + 1] - hoo[a], hgo[a + 1] - hgo[a]); };
+      for (int32_t a : big)
+        if (big_mx(a) > kWaveSmallMax) order.push_back(a);
+      for (int32_t a : big)
+        if (big_mx(a) <= kWaveSmallMax) order.push_back(a);
     }
     std::vector<int64_t> toff(order.size() + 1, 0);
     for (size_t k = 0; k < order.size(); ++k) {
@@ -1293,47 +1298,62 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     g.pre_off = pre.get() ? pre_off.get() : nullptr;
     std::vector<int32_t> lo;
     if (!aggs.empty()) launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, s);
-    DBuf<int32_t> big_list;
-    if (!big.empty()) {
-      const int base = static_cast<int>(lo.size());
-      const int cnt = static_cast<int>(big.size());
-      int64_t wmax = 0, nmax = 0;
+    // cluster classes: subdomains up to 256 run on 2-CTA clusters (16 replay warps cover
+    // their 2·NB row groups), larger ones on 4-CTA clusters
+    std::vector<DBuf<int32_t>> big_lists;
+    std::vector<DBuf<double>> big_ws;
+    std::vector<DBuf<WaveCtl>> big_ctl;
+    for (int pass = 0; pass < 2 && !big.empty(); ++pass) {
+      const int C = pass == 0 ? 4 : 2;
+      std::vector<int32_t> part;
       for (int32_t a : big) {
+        const int64_t mx = std::max(hoo[a + 1] - hoo[a], hgo[a + 1] - hgo[a]);
+        if ((mx > kWaveSmallMax) == (pass == 0)) part.push_back(a);
+      }
+      if (part.empty()) continue;
+      const int base = static_cast<int>(lo.size());
+      const int cnt = static_cast<int>(part.size());
+      int64_t wmax = 0, nmax = 0;
+      for (int32_t a : part) {
         wmax = std::max(wmax, need[a]);
         nmax = std::max<int64_t>(nmax, std::max(hoo[a + 1] - hoo[a], hgo[a + 1] - hgo[a]));
       }
       wmax = r2(wmax);
       const int64_t wws = r2(wave_ws_doubles(nmax));
       // one cluster per slot; bound the footprint to ~2 GiB
-      const int64_t slots = std::max<int64_t>(1, std::min<int64_t>({int64_t(cnt), int64_t(sm_count()) / kWaveCluster,
+      const int64_t slots = std::max<int64_t>(1, std::min<int64_t>({int64_t(cnt), int64_t(sm_count()) / C,
                                                                     (int64_t(1) << 28) / std::max<int64_t>(wmax + wws, 1)}));
-      big_list.upload(big, s);
-      DBuf<double> gws(slots * wmax, s), wbuf(slots * wws, s);
-      DBuf<WaveCtl> ctls(slots, s);
-      ctls.zero(s);
+      big_lists.emplace_back();
+      big_lists.back().upload(part, s);
+      big_ws.emplace_back(slots * wmax, s);
+      double* gws = big_ws.back().get();
+      big_ws.emplace_back(slots * wws, s);
+      double* wbuf = big_ws.back().get();
+      big_ctl.emplace_back(slots, s);
+      big_ctl.back().zero(s);
       GevpArgs gb = g;
-      gb.list = big_list.get();
+      gb.list = big_lists.back().get();
       gb.list_base = base;
       gb.n_list = cnt;
       gb.ws_stride = wmax;
-      gb.gws = gws.get();
+      gb.gws = gws;
       const size_t smem = size_t(kWaveSmemCap) * 8;
       LSB_CUDA(cudaFuncSetAttribute(k_gevp_wave, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
       cudaLaunchConfig_t cfg = {};
-      cfg.gridDim = dim3(static_cast<unsigned>(slots * kWaveCluster));
+      cfg.gridDim = dim3(static_cast<unsigned>(slots * C));
       cfg.blockDim = dim3(512);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
       cudaLaunchAttribute at[1];
       at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = kWaveCluster;
+      at[0].val.clusterDim.x = C;
       at[0].val.clusterDim.y = 1;
       at[0].val.clusterDim.z = 1;
       cfg.attrs = at;
       cfg.numAttrs = 1;
-      LSB_CUDA(cudaLaunchKernelEx(&cfg, k_gevp_wave, gb, ctls.get(), wbuf.get(), wws, static_cast<int>(kWaveMinN)));
+      LSB_CUDA(cudaLaunchKernelEx(&cfg, k_gevp_wave, gb, big_ctl.back().get(), wbuf, wws, static_cast<int>(kWaveMinN)));
       LSB_LAUNCH();
-      lo.insert(lo.end(), big.begin(), big.end());
+      lo.insert(lo.end(), part.begin(), part.end());
     }
     chunk_list[ci].upload(lo, s);
   }
