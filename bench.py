@@ -12,7 +12,11 @@ rtol 1e-8 with the V(1,1) cycle. Metric: unknowns/s = n / (T_setup + T_solve).
   in, x copied out inside the timed region).
 * ``--impl reference``: the reference's own CPU implementation (the
   unmodified headers compiled into oracle/_ref, else the C oracle) on the
-  host cores, one bounded sample of the same workload per host thread.
+  host cores, on the same 1024×1024 problem: its level-0 stages and the
+  level-0 work of the PCG iterations (the coarse levels, which the reference
+  cannot finish at this size, are left out — an upper bound for the CPU).
+  The GPU line carries the same stages as ``same_stages`` for a like-for-like
+  ratio.
 
 Multi-GPU: ``python -m torch.distributed.run --nproc-per-node N bench.py
 --gpus N`` runs N independent replicas (round 1 is
@@ -37,7 +41,6 @@ sys.path.insert(0, ROOT)
 
 METRIC = "AMG-DD setup+PCG solve unknowns/s"
 UNIT = "unknowns/s"
-SAMPLE_GRID = 384  # bounded CPU sample of config 2 (same generator and parameters, ~30 s single-threaded)
 
 
 def env_int(k, d):
@@ -134,69 +137,94 @@ def barrier_max(pg, value: float, device) -> float:
     return float(t.item())
 
 
-def run_reference(args) -> dict:
-    """The reference CPU path: bounded samples of config 2, all host threads."""
+# PCG iterations of the bench workload (what the GPU arm reports for it); the
+# reference arm multiplies its level-0 per-iteration time by this count
+WORKLOAD_ITERS = {("c2", 1024): 70}
+
+LEVEL0_STAGES = ("level-0 setup stages (A0 = G^T G, topology, build_smoother, all local GEVPs, P0, Galerkin G1/A1) "
+                 "+ per PCG iteration the level-0 operator and smoother applications (G p, G^T(G p), RAS, RAS-T)")
+
+
+def reference_checker():
     from oracle import refbind
-    from paper_2601_04112_b200 import configs
 
     try:
-        chk, kind = refbind.reference(), "reference"
-    except FileNotFoundError:
-        chk, kind = refbind.oracle(), "port"
-    grid = args.sample_grid
-    cfg = configs.config("c2", grid)
-    p = refbind.params_for(cfg)
+        return refbind.reference(), "reference"
+    except (FileNotFoundError, OSError):
+        return refbind.oracle(), "port"
+
+
+def reference_level0_step(chk, cfg, threads: int, iters: int) -> dict:
+    """The reference's own functions on the level-0 share of the workload at its
+    full grid (probe_levels = 1). The coarse levels are left out: the reference's
+    sequential Jacobi eigensolves on them take days at this size,
+    so the resulting unknowns/s is an upper bound for the CPU."""
+    from oracle import refbind
+    from paper_2601_04112_b200 import abi
+
+    os.environ["LSAMGDD_REF_THREADS"] = str(threads)
+    p = refbind.params_for(cfg, probe_levels=1)
+    t0 = time.perf_counter()
+    h = chk.setup(cfg, p)
+    t_setup = time.perf_counter() - t0
+    x = cfg.rhs
+    t0 = time.perf_counter()
+    y = h.spmv(x, 0, abi.EXPORT_G, False, nout=cfg.m)
+    h.spmv(y, 0, abi.EXPORT_G, True, nout=cfg.n)
+    e = h.schwarz_apply(x, 0, abi.RAS)
+    h.schwarz_apply(e, 0, abi.RAST)
+    t_iter = time.perf_counter() - t0
+    stages = {}
+    for nm, sec in h.timings():
+        stages[nm] = stages.get(nm, 0.0) + sec * 1e3
+    del h
+    return {"seconds": t_setup + iters * t_iter, "setup_ms": t_setup * 1e3, "iter_ms": t_iter * 1e3,
+            "stages_ms": {k: round(v, 1) for k, v in stages.items()}}
+
+
+def run_reference(args) -> dict:
+    """The reference CPU path on the bench workload's own grid: its level-0 share, all host threads."""
+    from paper_2601_04112_b200 import configs
+
+    chk, kind = reference_checker()
+    cfg = configs.config(args.config, args.grid)
+    grid = cfg.meta["grid"]
+    iters = WORKLOAD_ITERS.get((cfg.name, grid), 50)
     threads = max(1, min(os.cpu_count() or 1, 64))
-
-    def one_step():
-        def work():
-            h = chk.setup(cfg, p)
-            h.pcg(cfg.rhs, 1e-8, 1000)
-
-        ts = [threading.Thread(target=work) for _ in range(threads)]
-        t0 = time.perf_counter()
-        for t in ts:
-            t.start()
-        for t in ts:
-            t.join()
-        return time.perf_counter() - t0
-
     for _ in range(args.warmup):
-        one_step()
-    times = [one_step() for _ in range(args.steps)]
+        last = reference_level0_step(chk, cfg, threads, iters)
+    times = []
+    for _ in range(args.steps):
+        last = reference_level0_step(chk, cfg, threads, iters)
+        times.append(last["seconds"])
     ms = 1e3 * statistics.mean(times)
-    value = threads * cfg.n / (ms / 1e3)
+    value = cfg.n / (ms / 1e3)
+    sample = (f"{LEVEL0_STAGES} of the same {grid}x{grid} problem, {iters} iterations; the coarse levels are left out "
+              f"(the reference cannot finish them at this size), so this is an upper bound for the CPU; "
+              f"per-aggregate stages on {threads} host threads")
     return {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 0, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c2", "grid": grid, "n": cfg.n, "sample_of": "c2 1024x1024",
-                   "parallelism": f"{threads} independent single-threaded solves"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                         "sample": f"config-2 generator at {grid}x{grid} (n={cfg.n}), setup+PCG end to end, "
-                                   f"one per thread on {threads} threads"},
+        "config": {"workload": cfg.name, "grid": grid, "n": cfg.n, "m": cfg.m, "nnz_G": cfg.nnz,
+                   "parallelism": f"{threads} host threads over the independent aggregates",
+                   "setup_ms": last["setup_ms"], "iter_ms": last["iter_ms"], "stages_ms": last["stages_ms"],
+                   "pcg_iterations": iters},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
-def cpu_baseline_sample() -> dict:
-    from oracle import refbind
-    from paper_2601_04112_b200 import configs
-
-    try:
-        chk, kind = refbind.reference(), "reference"
-    except FileNotFoundError:
-        chk, kind = refbind.oracle(), "port"
-    cfg = configs.config("c2", SAMPLE_GRID)
-    p = refbind.params_for(cfg)
-    t0 = time.perf_counter()
-    h = chk.setup(cfg, p)
-    t1 = time.perf_counter()
-    _, rep = h.pcg(cfg.rhs, 1e-8, 1000)
-    t2 = time.perf_counter()
-    return {"value": cfg.n / (t2 - t0), "unit": UNIT, "cores": 1, "kind": kind,
-            "sample": f"config-2 generator at {SAMPLE_GRID}x{SAMPLE_GRID} (n={cfg.n}), setup {t1 - t0:.2f}s + "
-                      f"PCG {t2 - t1:.2f}s ({rep['iterations']} it), single-threaded reference"}
+def cpu_baseline_sample(cfg, iters: int) -> dict:
+    chk, kind = reference_checker()
+    threads = max(1, min(os.cpu_count() or 1, 64))
+    r = reference_level0_step(chk, cfg, threads, iters)
+    return {"value": cfg.n / r["seconds"], "unit": UNIT, "cores": threads, "kind": kind,
+            "sample": f"{LEVEL0_STAGES} of the same {cfg.meta['grid']}x{cfg.meta['grid']} problem, {iters} iterations, "
+                      f"{threads} host threads: setup stages {r['setup_ms'] / 1e3:.2f} s + {iters} x {r['iter_ms']:.1f} ms; "
+                      f"coarse levels left out (upper bound for the CPU)",
+            "level0_ms": r["seconds"] * 1e3, "setup_ms": r["setup_ms"], "iter_ms": r["iter_ms"],
+            "stages_ms": r["stages_ms"]}
 
 
 def main() -> None:
@@ -208,8 +236,6 @@ def main() -> None:
     ap.add_argument("--config", default="c2")
     ap.add_argument("--grid", type=int, default=None, help="override the grid (debug only; not a bench number)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--sample-grid", type=int, default=SAMPLE_GRID,
-                    help="grid of the CPU reference sample (the default is the documented bench sample)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -278,8 +304,10 @@ def main() -> None:
         lib.lsamgdd_setup_timings(h, names, ms, C.c_int64(64), C.byref(cnt))
         setup_ms = sum(ms[i] for i in range(min(cnt.value, 64)))
         stages = {}
+        stages_list = []
         for i in range(min(cnt.value, 64)):
             stages[names[i].decode()] = stages.get(names[i].decode(), 0.0) + ms[i]
+            stages_list.append((names[i].decode(), ms[i]))
         summ = []
         nl = C.c_int64()
         lib.lsamgdd_num_levels(h, C.byref(nl))
@@ -287,7 +315,8 @@ def main() -> None:
         lib.lsamgdd_operator_complexity(h, C.byref(oc))
         lib.lsamgdd_destroy(h)
         return {"iterations": rep.iterations, "converged": bool(rep.converged), "setup_ms": setup_ms,
-                "solve_ms": rep.solve_seconds * 1e3, "levels": nl.value, "opcx": oc.value, "stages": stages}
+                "solve_ms": rep.solve_seconds * 1e3, "levels": nl.value, "opcx": oc.value, "stages": stages,
+                "stages_list": stages_list}
 
     def timed(device_inputs: bool, k: int, stats=None):
         times, infos = [], []
@@ -367,9 +396,27 @@ def main() -> None:
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    # the same stages on the GPU: level-0 setup stage timers + per-iteration event times of the
+    # operator pair and the Schwarz pair (measured inside the captured PCG graph)
+    st0 = infos[-1]["stages_list"]
+    lvl0 = {}
+    seen = set()
+    for nm, v in st0:
+        if nm in seen:
+            break  # the stage names repeat from level 1 on
+        seen.add(nm)
+        lvl0[nm] = v
+    it = max(int(ks.spmv_launches) // 2, 1)  # graph-launched iterations the event times were summed over
+    gpu_iter_ms = (ks.schwarz_ms + ks.spmv_ms) / it
+    gpu_level0_ms = sum(lvl0.values()) + infos[-1]["iterations"] * gpu_iter_ms
+    out["same_stages"] = {"stages": LEVEL0_STAGES, "gpu_ms": gpu_level0_ms, "gpu_setup_ms": sum(lvl0.values()),
+                          "gpu_iter_ms": gpu_iter_ms, "gpu_stages_ms": {k: round(v, 2) for k, v in lvl0.items()}}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            out["cpu_baseline"] = cpu_baseline_sample()
+            out["cpu_baseline"] = cpu_baseline_sample(cfg, int(infos[-1]["iterations"]))
+            out["same_stages"]["cpu_ms"] = out["cpu_baseline"]["level0_ms"]
+            out["same_stages"]["cpu_cores"] = out["cpu_baseline"]["cores"]
+            out["same_stages"]["ratio"] = out["cpu_baseline"]["level0_ms"] / gpu_level0_ms
         except Exception as e:  # the checker is test infrastructure; report its absence
             out["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                                    "sample": f"unavailable: {e}"}

@@ -19,6 +19,13 @@
  *  - A hierarchy handle is immutable after lsamgdd_setup and may be shared by
  *    concurrent vcycle/pcg/schwarz calls (hierarchy.hpp:56-57): each call uses
  *    its own stream and workspace.
+ *  - Device-memory arguments (lsamgdd_memory == LSAMGDD_DEVICE): the library
+ *    runs on its own non-blocking CUDA streams. Before it first reads such an
+ *    argument a call waits for the caller's pending device work: for the
+ *    stream registered with lsamgdd_set_caller_stream (per host thread), or,
+ *    when none is registered, for the whole device (cudaDeviceSynchronize).
+ *    Every call returns with its outputs complete (the library's stream is
+ *    synchronised), so the caller may read them from any stream.
  *  - There is no CPU fallback: on a machine without a usable sm_100 device,
  *    every compute entry point fails with LSAMGDD_ERR_CUDA.
  */
@@ -89,7 +96,11 @@ typedef struct lsamgdd_params {
   int32_t device;              /* CUDA ordinal, default 0 */
   double thresh_override;      /* <= 0: eigen_threshold (splitting.hpp:170); > 0: direct threshold on every level */
   uint64_t level0_max_modes;   /* 0: reference (cap = |omega| at level 0, hierarchy.hpp:156-157) */
-  uint64_t reserved[4];
+  uint64_t probe_levels;       /* 0: full setup. k > 0 (stage-wise parity and timing of the fine levels at full
+                                  size): build k levels with interpolation and the operators of level k, then stop
+                                  without factoring the coarsest level. Such a handle serves exports, level_spmv and
+                                  schwarz_apply on levels < k; vcycle and pcg fail with InputError. */
+  uint64_t reserved[3];
 } lsamgdd_params;
 
 /* LevelSummary (hierarchy.hpp:32-41). */
@@ -140,6 +151,10 @@ int32_t lsamgdd_abi_version(void);
 /* 1 if a usable sm_100 device is visible, else 0 (no error). */
 int32_t lsamgdd_device_available(void);
 
+/* Registers (enable != 0) or clears the CUDA stream (a cudaStream_t) on which
+ * the calling host thread produces device-memory arguments; see Conventions. */
+int lsamgdd_set_caller_stream(void* stream, int32_t enable);
+
 /* setup(g0, params)                                    hierarchy.hpp:106 */
 int lsamgdd_setup(const lsamgdd_csr* g0, const lsamgdd_params* params, void** out_handle,
                   char* err, size_t errlen);
@@ -164,6 +179,23 @@ int lsamgdd_pcg(const void* handle, const lsamgdd_csr* g, const double* b, doubl
 /* spmv(A_l or G_l or P_l, x) and spmv_transpose       sparse.hpp:110, :125 */
 int lsamgdd_level_spmv(const void* handle, int64_t level, int32_t what, int32_t transpose,
                        const double* x, double* y, int32_t memory, char* err, size_t errlen);
+
+/* ---- the sparse kernels on caller matrices (no hierarchy needed) ---- */
+/* spmv(a, x) (transpose == 0, sparse.hpp:110) or spmv_transpose(a, x)
+ * (sparse.hpp:125): row sums in CSR order, bit-identical to the reference. */
+int lsamgdd_spmv(const lsamgdd_csr* a, int32_t transpose, const double* x, double* y,
+                 int32_t memory, char* err, size_t errlen);
+/* spgemm(a, b, SpgemmMode::Symbolic) (sparse.hpp:167-204): the structural
+ * pattern with exact zeros kept, accumulated over k in the reference's order.
+ * The product stays on the device behind *out_matrix. */
+int lsamgdd_spgemm(const lsamgdd_csr* a, const lsamgdd_csr* b, void** out_matrix, char* err,
+                   size_t errlen);
+/* transpose(a) (sparse.hpp:139-153), stable in the source row order. */
+int lsamgdd_transpose(const lsamgdd_csr* a, void** out_matrix, char* err, size_t errlen);
+/* Host copy of a device matrix: sizes {rows, cols, nnz}; NULL arrays to query. */
+int lsamgdd_matrix_export(const void* matrix, int64_t sizes[3], int64_t* offsets, int64_t* cols,
+                          double* vals);
+int lsamgdd_matrix_destroy(void* matrix);
 
 /* Host mirrors (two-call protocol: pass NULL arrays to query sizes). */
 int lsamgdd_level_export(const void* handle, int64_t level, int32_t what, int64_t sizes[3],
@@ -190,8 +222,11 @@ int lsamgdd_profile_pcg(const void* handle, const double* b, double tol, uint64_
 
 /* sym_eig (eigen.hpp:35-118) of one dense n×n row-major matrix through a
  * device path of the batched eigensolver: 0 warp team, 1 CTA team, 2 CTA
- * pipelined (TMA-prefetched rows). Values ascending, vectors column k. Used by
- * the parity tests to pin each path bit-for-bit against the reference. */
+ * producer/consumer pipeline (cp.async-prefetched rows), 3 CTA pipeline with
+ * one barrier per rotation, 4 thread-block-cluster wavefront (tiles staged by
+ * 1-D bulk/TMA copies, rotation-log replay on helper CTAs; 2 <= n <= 608).
+ * Values ascending, vectors column k. Used by the parity tests to pin each
+ * path bit-for-bit against the reference. */
 int lsamgdd_dense_sym_eig(int64_t n, const double* a, double* values, double* vectors, int32_t path, char* err,
                           size_t errlen);
 

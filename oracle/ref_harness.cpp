@@ -13,9 +13,14 @@
 // hook active the replica makes exactly the reference's calls in the
 // reference's order (pinned by tests/test_oracle_pins.py against setup()).
 #include <algorithm>
+#include <atomic>
 #include <chrono>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <random>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -95,7 +100,7 @@ LevelParams to_params(const lsamgdd_params* p) {
 
 bool hooks_active(const lsamgdd_params* p) {
   return p->level0_partition != nullptr || p->level0_overlap >= 2 || p->thresh_override > 0.0 ||
-         p->level0_max_modes > 0;
+         p->level0_max_modes > 0 || p->probe_levels > 0;
 }
 
 // Second Γ layer: every node within graph distance 2 of omega_i, outside it,
@@ -155,6 +160,65 @@ double secs_since(std::chrono::steady_clock::time_point t0) {
   return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 }
 
+int ref_threads() {
+  if (const char* e = std::getenv("LSAMGDD_REF_THREADS")) return std::max(1, std::atoi(e));
+  return 1;
+}
+
+// Runs f(i) for i in [0, n) on LSAMGDD_REF_THREADS host threads (chunks of 64,
+// first exception rethrown); one thread by default, like the reference.
+template <class F>
+void for_each_aggregate(std::size_t n, F&& f) {
+  const int n_thr = ref_threads();
+  if (n_thr <= 1 || n < 64) {
+    for (std::size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<std::size_t> next{0};
+  std::exception_ptr first_err;
+  std::mutex err_mu;
+  std::vector<std::thread> pool;
+  for (int w = 0; w < n_thr; ++w)
+    pool.emplace_back([&] {
+      try {
+        for (;;) {
+          const std::size_t i0 = next.fetch_add(64);
+          if (i0 >= n) break;
+          for (std::size_t i = i0; i < std::min(n, i0 + 64); ++i) f(i);
+        }
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(err_mu);
+        if (!first_err) first_err = std::current_exception();
+      }
+    });
+  for (auto& th : pool) th.join();
+  if (first_err) std::rethrow_exception(first_err);
+}
+
+// build_smoother (smoother.hpp:38-58): the reference's own function on one
+// thread; with LSAMGDD_REF_THREADS > 1 its per-aggregate body (subdomain,
+// submatrix, factor_spd_block — the reference's functions, unchanged) runs
+// on several host threads. The factors do not depend on the order.
+SchwarzSmoother threaded_build_smoother(const SparseMatrix& a, const AggregateTopology& topo) {
+  if (ref_threads() <= 1) return build_smoother(a, topo, SchwarzMode::RAS);
+  if (a.n_rows() != a.n_cols()) throw DimError("build_smoother: matrix is not square");
+  if (a.n_rows() != topo.n_nodes) throw DimError("build_smoother: topology does not cover the matrix");
+  SchwarzSmoother s;
+  s.mode = SchwarzMode::RAS;
+  s.n = a.n_rows();
+  const std::size_t n_agg = topo.n_aggregates();
+  s.subdomains.resize(n_agg);
+  s.omega_sizes.resize(n_agg);
+  s.factors.resize(n_agg);
+  for_each_aggregate(n_agg, [&](std::size_t i) {
+    s.subdomains[i] = topo.subdomain(i);
+    s.omega_sizes[i] = topo.omega[i].size();
+    const DenseMatrix block = submatrix(a, s.subdomains[i], s.subdomains[i]);
+    s.factors[i] = factor_spd_block(block, "subdomain block of aggregate " + std::to_string(i));
+  });
+  return s;
+}
+
 // Stage replica of setup() (hierarchy.hpp:106-200) with the config hooks.
 void replica_setup(RefHandle& rh, const lsamgdd_params* cp) {
   const LevelParams params = to_params(cp);
@@ -178,7 +242,9 @@ void replica_setup(RefHandle& rh, const lsamgdd_params* cp) {
   h.levels.push_back(std::move(level));
   rh.timings.push_back({"galerkin_A0", secs_since(t)});
 
-  while (h.levels.size() < params.max_levels && h.levels.back().A.n_rows() > params.coarse_size) {
+  const std::size_t probe = static_cast<std::size_t>(cp->probe_levels);
+  while (h.levels.size() < params.max_levels && h.levels.back().A.n_rows() > params.coarse_size &&
+         (probe == 0 || h.levels.size() <= probe)) {
     const std::size_t ell = h.levels.size() - 1;
     Level& cur = h.levels.back();
     t = std::chrono::steady_clock::now();
@@ -195,7 +261,7 @@ void replica_setup(RefHandle& rh, const lsamgdd_params* cp) {
     if (ell == 0 && cp->level0_overlap >= 2) widen_overlap(cur.A, part, cur.topology);
     rh.timings.push_back({"aggregation_topology", secs_since(t)});
     t = std::chrono::steady_clock::now();
-    cur.smoother = build_smoother(cur.A, cur.topology, SchwarzMode::RAS);
+    cur.smoother = threaded_build_smoother(cur.A, cur.topology);
     rh.timings.push_back({"build_smoother", secs_since(t)});
     t = std::chrono::steady_clock::now();
     const RowSets rs = compute_row_sets(cur.G, cur.topology);
@@ -209,7 +275,11 @@ void replica_setup(RefHandle& rh, const lsamgdd_params* cp) {
     rh.spectra.emplace_back();
     auto& spec = rh.spectra.back();
     if (cp->keep_spectra) spec.resize(cur.topology.n_aggregates());
-    for (std::size_t i = 0; i < cur.topology.n_aggregates(); ++i) {
+    // The per-aggregate problems are independent (splitting.hpp:200-275 reads shared
+    // data only); LSAMGDD_REF_THREADS > 1 runs the reference's own functions on
+    // several host threads (the reference-arm timing). The default is the
+    // reference's single thread.
+    auto one = [&](std::size_t i) {
       const LocalBlocks blocks = assemble_local(i, cur.G, cur.topology, rs);
       std::size_t cap = cur.topology.omega[i].size();
       if (ell > 0) {
@@ -220,7 +290,8 @@ void replica_setup(RefHandle& rh, const lsamgdd_params* cp) {
       }
       panels[i] = local_gevp(i, blocks, cur.thresh, cap, params.gevp_variant,
                              cp->keep_spectra ? &spec[i] : nullptr, params.must_keep);
-    }
+    };
+    for_each_aggregate(cur.topology.n_aggregates(), one);
     rh.timings.push_back({"local_gevp", secs_since(t)});
     t = std::chrono::steady_clock::now();
     cur.P = assemble_P(cur.topology, panels);
@@ -246,8 +317,10 @@ void replica_setup(RefHandle& rh, const lsamgdd_params* cp) {
   }
   t = std::chrono::steady_clock::now();
   const Level& coarse = h.levels.back();
-  h.coarse_factor = factor_spd_block(to_dense(coarse.A), "coarsest-level matrix");
-  rh.timings.push_back({"coarse_factor", secs_since(t)});
+  if (probe == 0) {  // probe_levels: stage-wise runs of the fine levels stop before the dense coarsest factor
+    h.coarse_factor = factor_spd_block(to_dense(coarse.A), "coarsest-level matrix");
+    rh.timings.push_back({"coarse_factor", secs_since(t)});
+  }
   LevelSummary last;
   last.level = h.levels.size() - 1;
   last.dim = coarse.A.n_rows();

@@ -62,7 +62,8 @@ class Params(C.Structure):
         ("device", C.c_int32),
         ("thresh_override", C.c_double),
         ("level0_max_modes", C.c_uint64),
-        ("reserved", C.c_uint64 * 4),
+        ("probe_levels", C.c_uint64),
+        ("reserved", C.c_uint64 * 3),
     ]
 
 
@@ -128,6 +129,7 @@ def default_params(**over) -> Params:
     p.device = 0
     p.thresh_override = 0.0
     p.level0_max_modes = 0
+    p.probe_levels = 0
     for k, v in over.items():
         if k == "coarsening_ratios":
             p.n_ratios = len(v)

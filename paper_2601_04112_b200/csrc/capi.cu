@@ -58,19 +58,40 @@ const Hierarchy& H(const void* h) {
   return *static_cast<const Hierarchy*>(h);
 }
 
-// Runs f(d_in, d_out) on device vectors, staging host arrays when needed.
-template <class F>
-void with_vectors(const SolveWs& ws, const double* in, int64_t nin, double* out, int64_t nout, int32_t memory, F&& f) {
-  if (memory == LSAMGDD_DEVICE) {
-    f(in, out);
-    LSB_CUDA(cudaStreamSynchronize(ws.s));
+// ---- ordering against the caller's device work ---------------------------------
+// The library works on its own non-blocking streams. Device-memory inputs may
+// still be in flight on a caller stream, so before the first read the call
+// either waits on that stream (lsamgdd_set_caller_stream, per host thread) or,
+// when none was given, synchronises the device.
+thread_local cudaStream_t t_caller_stream = nullptr;
+thread_local bool t_has_caller_stream = false;
+
+void wait_for_caller(cudaStream_t lib_stream) {
+  if (!t_has_caller_stream) {
+    LSB_CUDA(cudaDeviceSynchronize());
     return;
   }
-  DBuf<double> din(std::max<int64_t>(nin, 1), ws.s), dout(std::max<int64_t>(nout, 1), ws.s);
-  if (nin) LSB_CUDA(cudaMemcpyAsync(din.get(), in, nin * 8, cudaMemcpyHostToDevice, ws.s));
+  cudaEvent_t ev;
+  LSB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  LSB_CUDA(cudaEventRecord(ev, t_caller_stream));
+  LSB_CUDA(cudaStreamWaitEvent(lib_stream, ev, 0));
+  LSB_CUDA(cudaEventDestroy(ev));
+}
+
+// Runs f(d_in, d_out) on device vectors, staging host arrays when needed.
+template <class F>
+void with_vectors(cudaStream_t ws_s, const double* in, int64_t nin, double* out, int64_t nout, int32_t memory, F&& f) {
+  if (memory == LSAMGDD_DEVICE) {
+    wait_for_caller(ws_s);
+    f(in, out);
+    LSB_CUDA(cudaStreamSynchronize(ws_s));  // results are complete when the call returns
+    return;
+  }
+  DBuf<double> din(std::max<int64_t>(nin, 1), ws_s), dout(std::max<int64_t>(nout, 1), ws_s);
+  if (nin) LSB_CUDA(cudaMemcpyAsync(din.get(), in, nin * 8, cudaMemcpyHostToDevice, ws_s));
   f(din.get(), dout.get());
-  if (nout) LSB_CUDA(cudaMemcpyAsync(out, dout.get(), nout * 8, cudaMemcpyDeviceToHost, ws.s));
-  LSB_CUDA(cudaStreamSynchronize(ws.s));
+  if (nout) LSB_CUDA(cudaMemcpyAsync(out, dout.get(), nout * 8, cudaMemcpyDeviceToHost, ws_s));
+  LSB_CUDA(cudaStreamSynchronize(ws_s));
 }
 
 void fill_report(lsamgdd_report* rep, const Hierarchy& h, const PcgResult& pr) {
@@ -118,6 +139,7 @@ int run_pcg(const void* handle, const lsamgdd_csr* g, const double* b, double to
     const Sell* gts = &h.g0t_sell;
     if (g) {
       DevCsr dg, dgt;
+      if (g->memory == LSAMGDD_DEVICE) wait_for_caller(ws.s);
       csr_upload(dg, g, ws.s);
       csr_transpose(dg, dgt, ws.s);
       sell_from_csr(dg, own_g, ws.s);
@@ -127,7 +149,7 @@ int run_pcg(const void* handle, const lsamgdd_csr* g, const double* b, double to
     }
     const int64_t n = gts->nr;
     PcgResult pr;
-    with_vectors(ws, b, n, x, n, memory, [&](const double* db, double* dx) {
+    with_vectors(ws.s, b, n, x, n, memory, [&](const double* db, double* dx) {
       pr = pcg(h, ws, *gs, *gts, db, dx, tol, maxit, stats);
     });
     fill_report(report, h, pr);
@@ -167,8 +189,21 @@ int lsamgdd_setup(const lsamgdd_csr* g0, const lsamgdd_params* params, void** ou
       lsamgdd_params_default(&p);
     lsb::validate_setup(g0, &p);  // host-side InputError contract first (hierarchy.hpp:107-117)
     require_device();
+    if (g0->memory == LSAMGDD_DEVICE) {  // setup reads the factor on its own stream
+      LSB_CUDA(cudaSetDevice(p.device));
+      if (t_has_caller_stream)
+        LSB_CUDA(cudaStreamSynchronize(t_caller_stream));
+      else
+        LSB_CUDA(cudaDeviceSynchronize());
+    }
     *out = lsb::setup(g0, &p);
   });
+}
+
+int lsamgdd_set_caller_stream(void* stream, int32_t enable) {
+  t_caller_stream = static_cast<cudaStream_t>(stream);
+  t_has_caller_stream = enable != 0;
+  return LSAMGDD_OK;
 }
 
 int lsamgdd_destroy(void* handle) {
@@ -200,7 +235,7 @@ int lsamgdd_vcycle(const void* handle, int64_t level, const double* r, double* e
     const Level& L = level_of(h, level);
     SolveWs ws(h);
     const int64_t n = L.A.nr;
-    with_vectors(ws, r, n, e, n, memory, [&](const double* dr, double* de) { vcycle(h, ws, level, dr, de); });
+    with_vectors(ws.s, r, n, e, n, memory, [&](const double* dr, double* de) { vcycle(h, ws, level, dr, de); });
   });
 }
 
@@ -215,7 +250,7 @@ int lsamgdd_schwarz_apply(const void* handle, int64_t level, int32_t mode, const
       raise(LSAMGDD_ERR_INPUT, "schwarz: only RAS and RAS-T are built on the device (ASM is out of scope)");
     SolveWs ws(h);
     const int64_t n = L.A.nr;
-    with_vectors(ws, r, n, e, n, memory, [&](const double* dr, double* de) {
+    with_vectors(ws.s, r, n, e, n, memory, [&](const double* dr, double* de) {
       const SchwarzView sv = L.schwarz_view();
       if (mode == LSAMGDD_RAS) {
         schwarz_ras(sv, dr, de, false, ws.s);
@@ -249,7 +284,7 @@ int lsamgdd_level_spmv(const void* handle, int64_t level, int32_t what, int32_t 
       const InterpView iv = L.interp_view();
       const int64_t nin = transpose ? iv.n_fine : iv.n_coarse;
       const int64_t nout = transpose ? iv.n_coarse : iv.n_fine;
-      with_vectors(ws, x, nin, y, nout, memory, [&](const double* dx, double* dy) {
+      with_vectors(ws.s, x, nin, y, nout, memory, [&](const double* dx, double* dy) {
         if (transpose) {
           restrict_pt(iv, dx, dy, ws.s, /*exact=*/true);
         } else {
@@ -281,8 +316,123 @@ int lsamgdd_level_spmv(const void* handle, int64_t level, int32_t what, int32_t 
       }
     }
     const int64_t nin = sp->nc, nout = sp->nr;
-    with_vectors(ws, x, nin, y, nout, memory, [&](const double* dx, double* dy) { sell_spmv(*sp, dx, dy, nullptr, ws.s); });
+    with_vectors(ws.s, x, nin, y, nout, memory, [&](const double* dx, double* dy) { sell_spmv(*sp, dx, dy, nullptr, ws.s); });
   });
+}
+
+// ---- standalone sparse kernels on caller matrices (sparse.hpp:110-204) ----------
+
+namespace {
+struct OwnStream {
+  cudaStream_t s = nullptr;
+  OwnStream() { LSB_CUDA(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking)); }
+  ~OwnStream() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+struct MatrixHandle {
+  DevCsr m;
+  cudaStream_t s = nullptr;
+  ~MatrixHandle() {
+    if (s) {
+      cudaStreamSynchronize(s);
+      m = DevCsr();
+      cudaStreamSynchronize(s);
+      cudaStreamDestroy(s);
+    }
+  }
+};
+void check_csr(const lsamgdd_csr* a, const char* who) {
+  if (!a || a->n_rows < 0 || a->n_cols < 0 || a->nnz < 0 || (a->nnz > 0 && (!a->col_indices || !a->values)) ||
+      !a->row_offsets)
+    raise(LSAMGDD_ERR_INPUT, std::string(who) + ": malformed CSR argument");
+}
+}  // namespace
+
+int lsamgdd_spmv(const lsamgdd_csr* a, int32_t transpose, const double* x, double* y, int32_t memory, char* err,
+                 size_t errlen) {
+  return guarded(err, errlen, [&] {
+    check_csr(a, "spmv");
+    require_device();
+    OwnStream st;
+    if (a->memory == LSAMGDD_DEVICE) wait_for_caller(st.s);
+    DevCsr d;
+    csr_upload(d, a, st.s);
+    Sell sell;
+    if (transpose) {
+      DevCsr t;
+      csr_transpose(d, t, st.s);
+      sell_from_csr(t, sell, st.s);
+    } else {
+      sell_from_csr(d, sell, st.s);
+    }
+    with_vectors(st.s, x, sell.nc, y, sell.nr, memory,
+                 [&](const double* dx, double* dy) { sell_spmv(sell, dx, dy, nullptr, st.s); });
+  });
+}
+
+int lsamgdd_spgemm(const lsamgdd_csr* a, const lsamgdd_csr* b, void** out_matrix, char* err, size_t errlen) {
+  if (out_matrix) *out_matrix = nullptr;
+  return guarded(err, errlen, [&] {
+    check_csr(a, "spgemm");
+    check_csr(b, "spgemm");
+    if (!out_matrix) raise(LSAMGDD_ERR_INPUT, "spgemm: null output");
+    if (a->n_cols != b->n_rows)  // sparse.hpp:169-171
+      raise(LSAMGDD_ERR_DIM, "spgemm: inner dimensions " + std::to_string(a->n_cols) + " and " +
+                                 std::to_string(b->n_rows) + " differ");
+    require_device();
+    auto h = std::make_unique<MatrixHandle>();
+    LSB_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    if (a->memory == LSAMGDD_DEVICE || b->memory == LSAMGDD_DEVICE) wait_for_caller(h->s);
+    DevCsr da, db;
+    csr_upload(da, a, h->s);
+    csr_upload(db, b, h->s);
+    csr_spgemm_symbolic(da, db, h->m, h->s);
+    LSB_CUDA(cudaStreamSynchronize(h->s));
+    *out_matrix = h.release();
+  });
+}
+
+int lsamgdd_transpose(const lsamgdd_csr* a, void** out_matrix, char* err, size_t errlen) {
+  if (out_matrix) *out_matrix = nullptr;
+  return guarded(err, errlen, [&] {
+    check_csr(a, "transpose");
+    if (!out_matrix) raise(LSAMGDD_ERR_INPUT, "transpose: null output");
+    require_device();
+    auto h = std::make_unique<MatrixHandle>();
+    LSB_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    if (a->memory == LSAMGDD_DEVICE) wait_for_caller(h->s);
+    DevCsr da;
+    csr_upload(da, a, h->s);
+    csr_transpose(da, h->m, h->s);
+    LSB_CUDA(cudaStreamSynchronize(h->s));
+    *out_matrix = h.release();
+  });
+}
+
+int lsamgdd_matrix_export(const void* matrix, int64_t sizes[3], int64_t* offsets, int64_t* cols, double* vals) {
+  return guarded(nullptr, 0, [&] {
+    if (!matrix) raise(LSAMGDD_ERR_INPUT, "null matrix handle");
+    const MatrixHandle& h = *static_cast<const MatrixHandle*>(matrix);
+    sizes[0] = h.m.nr;
+    sizes[1] = h.m.nc;
+    sizes[2] = h.m.nnz;
+    if (!offsets && !cols && !vals) return;
+    std::vector<int64_t> off, col;
+    std::vector<double> val;
+    csr_download(h.m, off, col, val, h.s);
+    if (offsets) std::copy(off.begin(), off.end(), offsets);
+    if (cols) std::copy(col.begin(), col.end(), cols);
+    if (vals) std::copy(val.begin(), val.end(), vals);
+  });
+}
+
+int lsamgdd_matrix_destroy(void* matrix) {
+  delete static_cast<MatrixHandle*>(matrix);
+  return LSAMGDD_OK;
 }
 
 int lsamgdd_level_export(const void* handle, int64_t level, int32_t what, int64_t sizes[3], int64_t* idx0, int64_t* idx1,

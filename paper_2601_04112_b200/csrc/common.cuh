@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -114,6 +115,11 @@ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 // Number of SMs of the current device (148 on B200); grids are sized in
 // multiples of it.
 int sm_count();
+
+// True the first time it is called for the current device with this flag word
+// (one bit per device ordinal): guards per-device one-time settings such as
+// cudaFuncSetAttribute without process-wide booleans.
+bool first_on_device(std::atomic<uint64_t>& flags);
 
 #ifdef __CUDACC__
 // A cooperating group that runs one problem: a warp (lane-parallel,

@@ -361,15 +361,26 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
   h->ratios.assign(p->coarsening_ratios, p->coarsening_ratios + p->n_ratios);
   h->device = p->device;
   LSB_CUDA(cudaSetDevice(p->device));
-  {
-    // Keep freed stream-ordered memory mapped in the device pool: the setup
-    // allocates and frees hundreds of MB of per-level workspace, and returning
-    // it to the driver at every synchronisation costs seconds of remapping.
-    cudaMemPool_t pool;
-    LSB_CUDA(cudaDeviceGetDefaultMemPool(&pool, p->device));
-    uint64_t keep = UINT64_MAX;
-    LSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  }
+  // Keep freed stream-ordered memory mapped while this setup runs: it allocates
+  // and frees hundreds of MB of per-level workspace, and returning it to the
+  // driver at every synchronisation costs seconds of remapping. The host
+  // application's own threshold is put back when setup returns.
+  struct PoolKeep {
+    cudaMemPool_t pool = nullptr;
+    uint64_t old = 0;
+    explicit PoolKeep(int device) {
+      if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
+        pool = nullptr;
+        return;
+      }
+      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old);
+      uint64_t keep = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
+    ~PoolKeep() {
+      if (pool) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old);
+    }
+  } pool_keep(p->device);
   LSB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   cudaStream_t s = h->stream;
   auto stage = [&](const char* name, Clock::time_point t0) {
@@ -388,7 +399,9 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
     sell_from_csr(gt, h->g0t_sell, s);
   }
   stage("upload_galerkin_A0", t0);
-  while (h->levels.size() < p->max_levels && static_cast<uint64_t>(h->levels.back().A.nr) > p->coarse_size) {
+  const uint64_t probe = p->probe_levels;
+  while (h->levels.size() < p->max_levels && static_cast<uint64_t>(h->levels.back().A.nr) > p->coarse_size &&
+         (probe == 0 || h->levels.size() <= probe)) {
     const int64_t ell = static_cast<int64_t>(h->levels.size()) - 1;
     Level& cur = h->levels.back();
     t0 = Clock::now();
@@ -456,7 +469,8 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
   {
     const Level& co = h->levels.back();
     h->n_coarse = co.A.nr;
-    coarse_factor(co.A, h->coarse_inv, s);
+    h->probe = probe > 0;
+    if (!h->probe) coarse_factor(co.A, h->coarse_inv, s);
   }
   stage("coarse_factor", t0);
   lsamgdd_level_summary last{};
@@ -516,6 +530,7 @@ static void level_residual(const Level& L, const double* e, double* res, const d
 
 void vcycle(const Hierarchy& h, SolveWs& ws, int64_t level, const double* r, double* e) {
   if (level < 0 || level >= static_cast<int64_t>(h.levels.size())) raise(LSAMGDD_ERR_INDEX, "vcycle: level out of range");
+  if (h.probe) raise(LSAMGDD_ERR_INPUT, "vcycle: the hierarchy was built with probe_levels (no coarsest factorisation)");
   const Level& L = h.levels[level];
   cudaStream_t s = ws.s;
   const int64_t n = L.A.nr;
@@ -633,7 +648,15 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
       out.converged = true;
       break;
     }
-    if (k == maxit) break;
+    if (k == maxit) {
+      // krylov.hpp:75-77: the reference still applies the preconditioner after its last
+      // iteration and throws IndefiniteError on a non-positive <r, Br>
+      vcycle(h, ws, 0, r.get(), z.get());
+      pcg_rz(ws.red, r.get(), z.get(), n, sc.get(), false, s);
+      readback();
+      if (!(hsc->rz_next > 0.0)) raise(LSAMGDD_ERR_INDEFINITE, "pcg: preconditioned product <r, Br> is not positive");
+      break;
+    }
     LSB_CUDA(cudaGraphLaunch(gexec, s));
     ++graph_launches;
     readback();

@@ -47,6 +47,7 @@ struct Hierarchy {
   std::vector<Level> levels;
   DBuf<double> coarse_inv;
   int64_t n_coarse = 0;
+  bool probe = false;  // built with probe_levels: no coarsest factorisation, no cycles
   lsamgdd_params params{};
   std::vector<uint64_t> ratios;
   std::vector<lsamgdd_level_summary> summary;

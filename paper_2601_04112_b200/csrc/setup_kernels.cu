@@ -1115,11 +1115,14 @@ void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int3
     sm.max_omega = std::max(sm.max_omega, nw);
     sm.max_sub = std::max(sm.max_sub, nw + ng);
     const double blk = 8.0 * (nw * (nw + 1) / 2 + nw * ng);
-    b_ras += blk + 4.0 * (nw + ng) + 8.0 * (nw + ng) + 8.0 * nw;     // block + Ω ids + read r[Ω] + write e[ω]
-    b_rast += blk + 4.0 * (nw + ng) + 8.0 * nw + 16.0 * (nw + ng);   // block + Ω ids + read r[ω] + RMW e[Ω]
+    b_ras += blk + 4.0 * (nw + ng);   // block (ω columns of the inverse) + Ω index list
+    b_rast += blk + 4.0 * (nw + ng);
   }
-  sm.bytes_ras = b_ras;
-  sm.bytes_rast = b_rast;
+  // every vector entry counts once per sweep, however many
+  // subdomains gather it — RAS reads r and writes e (16 n), RAS-T reads r and
+  // read-modify-writes e (24 n)
+  sm.bytes_ras = b_ras + 16.0 * static_cast<double>(topo.n_nodes);
+  sm.bytes_rast = b_rast + 24.0 * static_cast<double>(topo.n_nodes);
   sm.off.upload(off, s);
   sm.data.alloc(off[na], s);
   DBuf<int32_t> status(na, s);
@@ -1154,6 +1157,8 @@ void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int3
   const int64_t max_blk = sm.max_omega * (sm.max_omega + 1) / 2 + sm.max_omega * (sm.max_sub - sm.max_omega);
   sm.rows = sm.n_groups == 0 && (max_blk > kRowsMinBlk || sm.max_sub > 512);
   if (sm.rows) build_row_layout(topo, hoo, hgo, byc, sm, s);
+  // the sweeps read only the lane or row layout built from the packed blocks
+  if (sm.rows || sm.n_groups > 0) sm.data.release();
 }
 
 void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int32_t>& hoo,

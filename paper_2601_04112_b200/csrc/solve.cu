@@ -7,6 +7,7 @@
 // memory with coalesced loads, then one lane per output row forms its dot
 // product. Grids are persistent, sized in multiples of the SM count.
 #include <algorithm>
+#include <atomic>
 
 #include "solve.cuh"
 
@@ -105,22 +106,18 @@ void schwarz_launch(const SchwarzView& v, const int32_t* list, int64_t count, co
     constexpr int WPB = 8;
     const int stage = static_cast<int>((max_blk + 1) & ~int64_t(1));
     const size_t smem = size_t(WPB) * (stage + rstage) * 8;
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set{0};  // per device (the attribute is per device)
+    if (first_on_device(attr_set))
       LSB_CUDA(cudaFuncSetAttribute(k_schwarz_warp<MODE, WPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-      attr_set = true;
-    }
     const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(8, (200 * 1024) / std::max<size_t>(smem, 1)));
     const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(count, WPB), sm_count() * per_sm)));
     k_schwarz_warp<MODE, WPB><<<grid, WPB * 32, smem, s>>>(v, list, count, r, e, stage, rstage);
   } else {
     const int stage = max_blk <= 24000 ? static_cast<int>((max_blk + 1) & ~int64_t(1)) : 0;
     const size_t smem = size_t(stage + rstage) * 8;
-    static bool attr_set_b = false;
-    if (!attr_set_b) {
+    static std::atomic<uint64_t> attr_set_b{0};
+    if (first_on_device(attr_set_b))
       LSB_CUDA(cudaFuncSetAttribute(k_schwarz_block<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-      attr_set_b = true;
-    }
     const int grid = static_cast<int>(std::min<int64_t>(count, int64_t(sm_count()) * 4));
     k_schwarz_block<MODE><<<grid, 256, smem, s>>>(v, list, count, r, e, stage, rstage);
   }
@@ -207,11 +204,9 @@ void schwarz_lane_launch(const SchwarzView& v, int64_t g_begin, int64_t g_end, c
   const int big = static_cast<int>(v.max_sub), small = static_cast<int>(v.max_omega);
   constexpr int WPB = 8;
   const size_t smem = size_t(WPB) * (big + small) * 32 * 8;
-  static bool attr = false;
-  if (!attr) {
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr))
     LSB_CUDA(cudaFuncSetAttribute(k_schwarz_lane<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-    attr = true;
-  }
   const int64_t per_sm = std::max<int64_t>(1, (220 * 1024) / std::max<size_t>(smem, 1));
   const int grid = static_cast<int>(std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(g_end - g_begin, WPB), int64_t(sm_count()) * std::min<int64_t>(per_sm, 8))));
@@ -284,11 +279,9 @@ __device__ __forceinline__ double lrow_fixed(const int32_t* __restrict__ ids, co
 
 // Launch with programmatic stream serialization (PDL): the kernel's
 // griddepcontrol.wait orders it after its predecessor, while its launch and
-// CTA rasterisation overlap the predecessor's drain. LSB_NO_PDL=1 disables
-// the attribute (the waits are then no-ops).
+// CTA rasterisation overlap the predecessor's drain.
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
-  static const bool pdl = getenv("LSB_NO_PDL") == nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -297,7 +290,7 @@ void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Arg
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl ? 1 : 0;
+  cfg.numAttrs = 1;
   LSB_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
@@ -393,7 +386,7 @@ void schwarz_lrow_launch(const SchwarzView& v, const int32_t* items, int64_t i0,
   if (i1 <= i0) return;
   // one full wave of resident CTAs (grid-stride over the items): a partial
   // last wave left most SMs idle during the drain (ncu: 3.2 waves for MODE 2)
-  static const int resident = [] {
+  const int resident = [] {  // per call: launches are captured once per solve, and the value is per device
     int b = 0;
     LSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_schwarz_lrow<MODE>, 256, 0));
     return std::max(b, 1);
@@ -610,16 +603,16 @@ void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t*
     LSB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, 256, 0));
     return std::max(b, 1);
   };
-  static const int res_rows = resident(k_schwarz_rows<MODE>);
+  const int res_rows = resident(k_schwarz_rows<MODE>);
   const int grid = static_cast<int>(
       std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_rows)));
   if (MODE < 2 && v.ras_ch > 1) {
-    static const int res_ch = resident(k_schwarz_rows_ch<MODE>);
+    const int res_ch = resident(k_schwarz_rows_ch<MODE>);
     const int g3 = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_ch)));
     launch_pdl(k_schwarz_rows_ch<MODE>, g3, 256, s, v, ia, ir, i0, i1, r, e);
   } else if (MODE == 2 && v.rast_ch > 1) {
-    static const int res_tch = resident(k_schwarz_rows_tch);
+    const int res_tch = resident(k_schwarz_rows_tch);
     const int g3 = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8), int64_t(sm_count()) * res_tch)));
     launch_pdl(k_schwarz_rows_tch, g3, 256, s, v, ia, ir, i0, i1, r, e);
@@ -627,7 +620,7 @@ void schwarz_rows_launch(const SchwarzView& v, const int32_t* ia, const int32_t*
     // lanes per row: 4 / 8 / 16 for nω up to 8 / 16 / 64 (≤ 4 entries per lane)
     const int lanes = v.max_omega <= 8 ? 4 : v.max_omega <= 16 ? 8 : 16;
     const int per_warp = 32 / lanes;
-    static const int res_t = std::min({resident(k_schwarz_rows_t<4>), resident(k_schwarz_rows_t<8>),
+    const int res_t = std::min({resident(k_schwarz_rows_t<4>), resident(k_schwarz_rows_t<8>),
                                        resident(k_schwarz_rows_t<16>)});
     const int g2 = static_cast<int>(
         std::max<int64_t>(1, std::min<int64_t>(ceil_div(i1 - i0, 8 * per_warp), int64_t(sm_count()) * res_t)));

@@ -245,12 +245,23 @@ void csr_spmv_warp(const DevCsr& a, const double* x, double* y, const double* r,
 }
 
 int sm_count() {
-  static int n = [] {
-    int dev = 0, v = 148;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-    return v;
-  }();
-  return n;
+  static std::atomic<int> cache[64];  // per device ordinal, 0 = not queried yet
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int v = cache[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    v = 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    cache[dev].store(v, std::memory_order_relaxed);
+  }
+  return v;
+}
+
+bool first_on_device(std::atomic<uint64_t>& flags) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return true;
+  const uint64_t bit = uint64_t(1) << dev;
+  return (flags.fetch_or(bit, std::memory_order_acq_rel) & bit) == 0;
 }
 
 void csr_upload(DevCsr& d, const lsamgdd_csr* h, cudaStream_t s) {

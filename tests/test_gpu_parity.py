@@ -354,3 +354,40 @@ def test_cpp_shim_drop_in(gpu):
         pytest.skip("shim_demo.bin not built (needs /root/reference at build time)")
     res = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+def _fixture(name):
+    import json
+    import os
+    path = os.path.join(os.path.dirname(__file__), "golden", name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated (scripts/make_level0_fixture.py needs the compiled reference)")
+    with open(path) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name,grid", [("c2", 1024), ("c3", 2048), ("c3", 4096)])
+def test_full_size_level0_matches_reference_hashes(gpu, name, grid):
+    """Stage-wise parity at the BASELINE grids: the level-0 stages (A₀, partition,
+    Γ sets, colours, multiplicities, per-aggregate spectra, P₀, G₁, A₁) built on
+    the GPU with probe_levels = 1 equal, bit for bit, what the compiled reference
+    (oracle/_ref) produced at the same grid (hashes committed under tests/golden
+    by scripts/make_level0_fixture.py; the reference cannot finish the coarse
+    levels at these sizes)."""
+    from . import _hashes
+    fx = _fixture(f"level0_{name}_{grid}.json")
+    cfg = configs.config(name, grid)
+    assert (cfg.n, cfg.m) == (fx["n"], fx["m"])
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg, keep_spectra=True, probe_levels=1))
+    assert h.num_levels == 2
+    for level, key in ((0, "level0"), (1, "level1")):
+        for stage, ref in fx[key].items():
+            sizes, arrays = _hashes.gpu_stage(h, level, stage)
+            assert sizes == ref["sizes"], (level, stage)
+            assert _hashes.digest(arrays) == ref["sha256"], (level, stage)
+    s0 = h.summary[0]
+    so = fx["summary0"]
+    assert (s0.dim, s0.nnz, s0.n_aggregates, s0.k_c, s0.n_mult, s0.modes_kept, s0.thresh) == (
+        so["dim"], so["nnz"], so["n_aggregates"], so["k_c"], so["n_mult"], so["modes_kept"], so["thresh"])
+    with pytest.raises(lsamgdd.InputError):
+        lsamgdd.vcycle(h, cfg.rhs)  # a probe handle has no coarsest factorisation
