@@ -192,6 +192,19 @@ int lsamgdd_spgemm(const lsamgdd_csr* a, const lsamgdd_csr* b, void** out_matrix
                    size_t errlen);
 /* transpose(a) (sparse.hpp:139-153), stable in the source row order. */
 int lsamgdd_transpose(const lsamgdd_csr* a, void** out_matrix, char* err, size_t errlen);
+/* build_smoother(a, topo) (smoother.hpp:38-58) on a caller operator and
+ * topology: omega/gamma are the aggregates' interior and boundary node lists
+ * (AggregateTopology, aggregation.hpp:33-40; the interiors partition the
+ * nodes), colors a proper colouring of the subdomain-intersection graph
+ * (aggregation.hpp:213-229). Concurrent applies on one smoother are not
+ * supported (it owns a single stream). */
+int lsamgdd_build_smoother(const lsamgdd_csr* a, int64_t n_aggregates, const int64_t* omega_offsets,
+                           const int64_t* omega, const int64_t* gamma_offsets, const int64_t* gamma,
+                           const int64_t* colors, void** out_smoother, char* err, size_t errlen);
+/* apply(smoother, r, mode) (smoother.hpp:65-83); mode LSAMGDD_RAS or LSAMGDD_RAST. */
+int lsamgdd_smoother_apply(const void* smoother, int32_t mode, const double* r, double* e,
+                           int32_t memory, char* err, size_t errlen);
+int lsamgdd_smoother_destroy(void* smoother);
 /* Host copy of a device matrix: sizes {rows, cols, nnz}; NULL arrays to query. */
 int lsamgdd_matrix_export(const void* matrix, int64_t sizes[3], int64_t* offsets, int64_t* cols,
                           double* vals);

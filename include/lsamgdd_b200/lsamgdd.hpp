@@ -13,6 +13,12 @@
 //   pcg(const Hierarchy&, const SparseMatrix& g, const Vector& b, tol, maxit)
 //                                  krylov.hpp:42 with apply_a = Gᵀ(G·), apply_b = vcycle
 //   operator_complexity(const Hierarchy&)                     hierarchy.hpp:257
+//   spmv / spmv_transpose / transpose / spgemm on caller matrices  sparse.hpp:110-204
+//   build_smoother(A, topo) + apply(smoother, r, mode)        smoother.hpp:38-83
+//   h.levels[l].{A, G, P, has_interpolation, topology, thresh}  hierarchy.hpp:46-53
+//   LevelParams::spectra_csv is honoured (hierarchy.hpp:121-127, :163-165)
+//   pcg(apply_a, apply_b, b, tol, maxit) with caller functors is the reference's
+//   own host loop (krylov.hpp:42), re-exported unchanged.
 //
 // Errors come back as the reference's own exception classes (same name(),
 // same what() text), so existing catch blocks keep working. The Hierarchy is
@@ -20,7 +26,9 @@
 #pragma once
 
 #include <cstring>
+#include <fstream>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <utility>
 #include <vector>
@@ -75,10 +83,37 @@ struct Extensions {  // the config hooks of lsamgdd_params (defaults = reference
   int device = 0;
 };
 
+class Hierarchy;
+
+// h.levels[l] — host mirrors of Level (hierarchy.hpp:46-53), fetched from the
+// device on first use and cached. `smoother` stays empty (the factors live on
+// the device; apply(h, level, r, mode) runs them).
+class LevelsView {
+ public:
+  explicit LevelsView(const Hierarchy* h = nullptr) : h_(h) {}
+  std::size_t size() const;
+  const Level& operator[](std::size_t l) const;
+  const Level& back() const { return (*this)[size() - 1]; }
+  const Level& front() const { return (*this)[0]; }
+
+ private:
+  const Hierarchy* h_;
+};
+
 class Hierarchy {
  public:
-  Hierarchy() = default;
-  explicit Hierarchy(void* h) : h_(h, &lsamgdd_destroy) {}
+  Hierarchy() : levels(this) {}
+  explicit Hierarchy(void* h) : levels(this), h_(h, &lsamgdd_destroy), cache_(std::make_shared<Cache>()) {}
+  Hierarchy(const Hierarchy& o) : levels(this), params(o.params), h_(o.h_), cache_(o.cache_) {}
+  Hierarchy(Hierarchy&& o) noexcept : levels(this), params(std::move(o.params)), h_(std::move(o.h_)), cache_(std::move(o.cache_)) {}
+  Hierarchy& operator=(Hierarchy o) {
+    params = std::move(o.params);
+    h_ = std::move(o.h_);
+    cache_ = std::move(o.cache_);
+    return *this;
+  }
+  LevelsView levels;   // h.levels[l].A / .G / .P / .topology / .thresh / .has_interpolation
+  LevelParams params;  // hierarchy.hpp:62
   void* handle() const { return h_.get(); }
   std::size_t num_levels() const {
     int64_t n = 0;
@@ -103,6 +138,64 @@ class Hierarchy {
     }
     return out;
   }
+  std::vector<int64_t> export_ints(std::size_t level, int what, int which, int64_t sz_out[3] = nullptr) const {
+    int64_t sz[3];
+    check(lsamgdd_level_export(h_.get(), static_cast<int64_t>(level), what, sz, nullptr, nullptr, nullptr), nullptr);
+    // sizes: PARTITION/COLORS/MULTIPLICITY {count, aux, 0}; GAMMA/SPECTRA {n_agg, total, 0}
+    std::vector<int64_t> a(which == 0 ? (what == LSAMGDD_EXPORT_GAMMA || what == LSAMGDD_EXPORT_SPECTRA ? sz[0] + 1 : sz[0])
+                                      : sz[1]);
+    check(lsamgdd_level_export(h_.get(), static_cast<int64_t>(level), what, sz, which == 0 ? a.data() : nullptr,
+                               which == 1 ? a.data() : nullptr, nullptr),
+          nullptr);
+    if (sz_out) std::memcpy(sz_out, sz, sizeof sz);
+    return a;
+  }
+  // per-aggregate eigenvalues of one level (keep_spectra / spectra_csv)
+  void spectra(std::size_t level, std::vector<int64_t>& off, std::vector<double>& vals) const {
+    int64_t sz[3];
+    check(lsamgdd_level_export(h_.get(), static_cast<int64_t>(level), LSAMGDD_EXPORT_SPECTRA, sz, nullptr, nullptr, nullptr),
+          nullptr);
+    off.assign(sz[0] + 1, 0);
+    vals.assign(sz[1], 0.0);
+    check(lsamgdd_level_export(h_.get(), static_cast<int64_t>(level), LSAMGDD_EXPORT_SPECTRA, sz, off.data(), nullptr,
+                               vals.data()),
+          nullptr);
+  }
+  const Level& level_mirror(std::size_t l) const {
+    std::lock_guard<std::mutex> lk(cache_->mu);
+    if (cache_->levels.size() < num_levels()) cache_->levels.resize(num_levels());
+    if (l >= cache_->levels.size()) throw IndexError("levels: index out of range");
+    auto& slot = cache_->levels[l];
+    if (!slot) {
+      auto lv = std::make_unique<Level>();
+      lv->A = level_matrix(l, LSAMGDD_EXPORT_A);
+      lv->G = level_matrix(l, LSAMGDD_EXPORT_G);
+      lv->has_interpolation = l + 1 < num_levels();
+      if (lv->has_interpolation) {
+        lv->P = level_matrix(l, LSAMGDD_EXPORT_P);
+        int64_t sz[3];
+        const std::vector<int64_t> asg = export_ints(l, LSAMGDD_EXPORT_PARTITION, 0, sz);
+        AggregateTopology& t = lv->topology;
+        t.n_nodes = asg.size();
+        t.omega.assign(static_cast<std::size_t>(sz[1]), {});
+        for (std::size_t v = 0; v < asg.size(); ++v) t.omega[static_cast<std::size_t>(asg[v])].push_back(v);
+        const std::vector<int64_t> goff = export_ints(l, LSAMGDD_EXPORT_GAMMA, 0);
+        const std::vector<int64_t> gnodes = export_ints(l, LSAMGDD_EXPORT_GAMMA, 1);
+        t.gamma.assign(t.omega.size(), {});
+        for (std::size_t i = 0; i < t.omega.size(); ++i)
+          t.gamma[i].assign(gnodes.begin() + goff[i], gnodes.begin() + goff[i + 1]);
+        const std::vector<int64_t> col = export_ints(l, LSAMGDD_EXPORT_COLORS, 0, sz);
+        t.colors.assign(col.begin(), col.end());
+        t.n_colors = static_cast<std::size_t>(sz[1]);
+        lsamgdd_level_summary s{};
+        check(lsamgdd_get_level_summary(h_.get(), static_cast<int64_t>(l), &s), nullptr);
+        t.multiplicity_max = s.n_mult;
+        lv->thresh = s.thresh;
+      }
+      slot = std::move(lv);
+    }
+    return *slot;
+  }
   // Host mirror of levels[l].A / .G / .P (hierarchy.hpp:46-51).
   SparseMatrix level_matrix(std::size_t level, int what) const {
     int64_t sz[3];
@@ -116,8 +209,16 @@ class Hierarchy {
   }
 
  private:
+  struct Cache {
+    std::mutex mu;
+    std::vector<std::unique_ptr<Level>> levels;
+  };
   std::shared_ptr<void> h_;
+  std::shared_ptr<Cache> cache_;
 };
+
+inline std::size_t LevelsView::size() const { return h_->num_levels(); }
+inline const Level& LevelsView::operator[](std::size_t l) const { return h_->level_mirror(l); }
 
 inline Hierarchy setup(const SparseMatrix& g0, const LevelParams& params, const Extensions& ext = {}) {
   lsamgdd_params p;
@@ -146,7 +247,22 @@ inline Hierarchy setup(const SparseMatrix& g0, const LevelParams& params, const 
   void* h = nullptr;
   char err[1024];
   check(lsamgdd_setup(&g.csr, &p, &h, err, sizeof err), err);
-  return Hierarchy(h);
+  Hierarchy out(h);
+  out.params = params;
+  if (!params.spectra_csv.empty()) {  // hierarchy.hpp:121-127, :163-165: level,aggregate,index,eigenvalue
+    std::ofstream spectra(params.spectra_csv);
+    if (!spectra) throw SetupError("setup: cannot open " + params.spectra_csv);
+    spectra.precision(17);
+    spectra << "level,aggregate,index,eigenvalue\n";
+    for (std::size_t ell = 0; ell + 1 < out.num_levels(); ++ell) {
+      std::vector<int64_t> off;
+      std::vector<double> vals;
+      out.spectra(ell, off, vals);
+      for (std::size_t i = 0; i + 1 < off.size(); ++i)
+        for (int64_t k = off[i]; k < off[i + 1]; ++k) spectra << ell << "," << i << "," << (k - off[i]) << "," << vals[k] << "\n";
+    }
+  }
+  return out;
 }
 
 inline Vector vcycle(const Hierarchy& h, std::size_t level, const Vector& r) {
@@ -189,6 +305,101 @@ inline std::pair<Vector, SolveReport> pcg(const Hierarchy& h, const SparseMatrix
   out.residual_history.assign(hist.begin(), hist.begin() + static_cast<std::ptrdiff_t>(rep.history_len));
   return {std::move(x), std::move(out)};
 }
+
+// ---- the sparse kernels on caller matrices (sparse.hpp:110-204) ----
+inline SparseMatrix from_device_matrix(void* m) {
+  std::unique_ptr<void, int (*)(void*)> guard(m, &lsamgdd_matrix_destroy);
+  int64_t sz[3];
+  check(lsamgdd_matrix_export(m, sz, nullptr, nullptr, nullptr), nullptr);
+  std::vector<int64_t> off(sz[0] + 1), col(sz[2]);
+  std::vector<double> val(sz[2]);
+  check(lsamgdd_matrix_export(m, sz, off.data(), col.data(), val.data()), nullptr);
+  return SparseMatrix(sz[0], sz[1], std::vector<std::size_t>(off.begin(), off.end()),
+                      std::vector<std::size_t>(col.begin(), col.end()), std::move(val));
+}
+
+inline Vector spmv(const SparseMatrix& a, const Vector& x) {
+  if (x.size() != a.n_cols())
+    throw DimError("spmv: vector length " + std::to_string(x.size()) + " does not match " + std::to_string(a.n_cols()) +
+                   " columns");
+  Vector y(a.n_rows());
+  CsrView v(a);
+  char err[1024];
+  check(lsamgdd_spmv(&v.csr, 0, x.data(), y.data(), LSAMGDD_HOST, err, sizeof err), err);
+  return y;
+}
+
+inline Vector spmv_transpose(const SparseMatrix& a, const Vector& x) {
+  if (x.size() != a.n_rows())
+    throw DimError("spmv_transpose: vector length " + std::to_string(x.size()) + " does not match " +
+                   std::to_string(a.n_rows()) + " rows");
+  Vector y(a.n_cols());
+  CsrView v(a);
+  char err[1024];
+  check(lsamgdd_spmv(&v.csr, 1, x.data(), y.data(), LSAMGDD_HOST, err, sizeof err), err);
+  return y;
+}
+
+inline SparseMatrix transpose(const SparseMatrix& a) {
+  CsrView v(a);
+  void* m = nullptr;
+  char err[1024];
+  check(lsamgdd_transpose(&v.csr, &m, err, sizeof err), err);
+  return from_device_matrix(m);
+}
+
+// Symbolic mode only (the hot path's mode; Numeric — exact zeros dropped — stays with the reference).
+inline SparseMatrix spgemm(const SparseMatrix& a, const SparseMatrix& b, SpgemmMode mode = SpgemmMode::Symbolic) {
+  if (mode != SpgemmMode::Symbolic) return lsamgdd::spgemm(a, b, mode);
+  CsrView va(a), vb(b);
+  void* m = nullptr;
+  char err[1024];
+  check(lsamgdd_spgemm(&va.csr, &vb.csr, &m, err, sizeof err), err);
+  return from_device_matrix(m);
+}
+
+// ---- build_smoother / apply on a caller operator (smoother.hpp:38-83) ----
+class Smoother {
+ public:
+  explicit Smoother(void* h, std::size_t n) : h_(h, &lsamgdd_smoother_destroy), n_(n) {}
+  void* handle() const { return h_.get(); }
+  std::size_t n() const { return n_; }
+
+ private:
+  std::shared_ptr<void> h_;
+  std::size_t n_;
+};
+
+inline Smoother build_smoother(const SparseMatrix& a, const AggregateTopology& topo, SchwarzMode = SchwarzMode::RAS) {
+  std::vector<int64_t> ooff{0}, om, goff{0}, gm, col(topo.colors.begin(), topo.colors.end());
+  for (std::size_t i = 0; i < topo.n_aggregates(); ++i) {
+    om.insert(om.end(), topo.omega[i].begin(), topo.omega[i].end());
+    ooff.push_back(static_cast<int64_t>(om.size()));
+    gm.insert(gm.end(), topo.gamma[i].begin(), topo.gamma[i].end());
+    goff.push_back(static_cast<int64_t>(gm.size()));
+  }
+  CsrView v(a);
+  void* h = nullptr;
+  char err[1024];
+  check(lsamgdd_build_smoother(&v.csr, static_cast<int64_t>(topo.n_aggregates()), ooff.data(), om.data(), goff.data(),
+                               gm.data(), col.data(), &h, err, sizeof err),
+        err);
+  return Smoother(h, a.n_rows());
+}
+
+inline Vector apply(const Smoother& s, const Vector& r, SchwarzMode mode) {
+  if (r.size() != s.n())
+    throw DimError("schwarz apply: vector length " + std::to_string(r.size()) + " does not match system size " +
+                   std::to_string(s.n()));
+  Vector e(r.size());
+  char err[1024];
+  const int m = mode == SchwarzMode::RAS ? LSAMGDD_RAS : mode == SchwarzMode::RAST ? LSAMGDD_RAST : LSAMGDD_ASM;
+  check(lsamgdd_smoother_apply(s.handle(), m, r.data(), e.data(), LSAMGDD_HOST, err, sizeof err), err);
+  return e;
+}
+
+// pcg with caller functors (krylov.hpp:42): the reference's host loop, unchanged
+using lsamgdd::pcg;
 
 inline double operator_complexity(const Hierarchy& h) {
   double v = 0.0;

@@ -251,7 +251,8 @@ int lsamgdd_schwarz_apply(const void* handle, int64_t level, int32_t mode, const
     SolveWs ws(h);
     const int64_t n = L.A.nr;
     with_vectors(ws.s, r, n, e, n, memory, [&](const double* dr, double* de) {
-      const SchwarzView sv = L.schwarz_view();
+      SchwarzView sv = L.schwarz_view();
+      sv.rast_done = ws.rast_done[level].get();
       if (mode == LSAMGDD_RAS) {
         schwarz_ras(sv, dr, de, false, ws.s);
       } else {
@@ -411,6 +412,36 @@ int lsamgdd_transpose(const lsamgdd_csr* a, void** out_matrix, char* err, size_t
     LSB_CUDA(cudaStreamSynchronize(h->s));
     *out_matrix = h.release();
   });
+}
+
+int lsamgdd_build_smoother(const lsamgdd_csr* a, int64_t n_aggregates, const int64_t* omega_offsets,
+                           const int64_t* omega, const int64_t* gamma_offsets, const int64_t* gamma,
+                           const int64_t* colors, void** out_smoother, char* err, size_t errlen) {
+  if (out_smoother) *out_smoother = nullptr;
+  return guarded(err, errlen, [&] {
+    check_csr(a, "build_smoother");
+    if (!out_smoother) raise(LSAMGDD_ERR_INPUT, "build_smoother: null output");
+    require_device();
+    if (a->memory == LSAMGDD_DEVICE) LSB_CUDA(cudaDeviceSynchronize());
+    *out_smoother = make_smoother(a, n_aggregates, omega_offsets, omega, gamma_offsets, gamma, colors);
+  });
+}
+
+int lsamgdd_smoother_apply(const void* smoother, int32_t mode, const double* r, double* e, int32_t memory, char* err,
+                           size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!smoother) raise(LSAMGDD_ERR_INPUT, "null smoother handle");
+    if (mode != LSAMGDD_RAS && mode != LSAMGDD_RAST)
+      raise(LSAMGDD_ERR_INPUT, "schwarz apply: this path implements RAS and RAST (ASM is a study mode)");
+    require_device();
+    const StandaloneSmoother& sm = *static_cast<const StandaloneSmoother*>(smoother);
+    with_vectors(sm.s, r, sm.n, e, sm.n, memory, [&](const double* dr, double* de) { smoother_apply(sm, mode, dr, de); });
+  });
+}
+
+int lsamgdd_smoother_destroy(void* smoother) {
+  delete static_cast<StandaloneSmoother*>(smoother);
+  return LSAMGDD_OK;
 }
 
 int lsamgdd_matrix_export(const void* matrix, int64_t sizes[3], int64_t* offsets, int64_t* cols, double* vals) {

@@ -311,6 +311,12 @@ SchwarzView Level::schwarz_view() const {
   v.n_lane_ras_items = static_cast<int64_t>(sm.lane_ras_items.size());
   v.lane_rast_items = sm.lane_rast_items.get();
   v.lane_rast_color_off = &sm.lane_rast_color_off;
+  v.g_color = sm.g_color.get();
+  v.color_groups = sm.color_groups.get();
+  v.rast_done = nullptr;  // the caller's workspace supplies the RAS-T counters
+  v.n_colors = static_cast<int>(sm.n_colors);
+  v.stage_blk_bytes = sm.stage_blk_bytes;
+  v.stage_ids_bytes = sm.stage_ids_bytes;
   v.rows = sm.rows;
   v.row_off = sm.row_off.get();
   v.row_data = sm.row_data.get();
@@ -482,6 +488,70 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
   return h.release();
 }
 
+StandaloneSmoother::~StandaloneSmoother() {
+  if (s) {
+    cudaStreamSynchronize(s);
+    rast_done.release();
+    L = Level();
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+  }
+}
+
+StandaloneSmoother* make_smoother(const lsamgdd_csr* a, int64_t n_agg, const int64_t* omega_off, const int64_t* omega,
+                                  const int64_t* gamma_off, const int64_t* gamma, const int64_t* colors) {
+  if (a->n_rows != a->n_cols) raise(LSAMGDD_ERR_DIM, "build_smoother: matrix is not square");
+  if (n_agg <= 0 || !omega_off || !omega || !gamma_off || !colors)
+    raise(LSAMGDD_ERR_INPUT, "build_smoother: topology arrays are required");
+  const int64_t n = a->n_rows;
+  if (omega_off[n_agg] != n)
+    raise(LSAMGDD_ERR_DIM, "build_smoother: topology covers " + std::to_string(omega_off[n_agg]) + " nodes, matrix has " +
+                               std::to_string(n));
+  auto sm = std::make_unique<StandaloneSmoother>();
+  sm->n = n;
+  LSB_CUDA(cudaStreamCreateWithFlags(&sm->s, cudaStreamNonBlocking));
+  Level& L = sm->L;
+  L.h_omega_off.assign(omega_off, omega_off + n_agg + 1);
+  L.h_omega.assign(omega, omega + n);
+  L.h_gamma_off.assign(gamma_off, gamma_off + n_agg + 1);
+  L.h_gamma.assign(gamma, gamma + gamma_off[n_agg]);
+  L.colors.assign(colors, colors + n_agg);
+  L.n_colors = 0;
+  for (int64_t c : L.colors) {
+    if (c < 0) raise(LSAMGDD_ERR_INPUT, "build_smoother: negative colour");
+    L.n_colors = std::max(L.n_colors, c + 1);
+  }
+  std::vector<int64_t> asg(n, -1);
+  for (int64_t i = 0; i < n_agg; ++i)
+    for (int64_t p = omega_off[i]; p < omega_off[i + 1]; ++p) {
+      if (omega[p] < 0 || omega[p] >= n || asg[omega[p]] != -1)
+        raise(LSAMGDD_ERR_INPUT, "build_smoother: the interiors must partition the nodes");
+      asg[omega[p]] = i;
+    }
+  for (int64_t k = 0; k < gamma_off[n_agg]; ++k)
+    if (gamma[k] < 0 || gamma[k] >= n) raise(LSAMGDD_ERR_INDEX, "build_smoother: boundary node out of range");
+  csr_upload(L.A, a, sm->s);
+  upload_topology(L, asg, sm->s);
+  build_smoother(L.A, L.topo, L.h_omega_off, L.h_gamma_off, L.colors, L.n_colors, L.sm, sm->s);
+  if (L.sm.n_groups > 0) {
+    sm->rast_done.alloc(L.sm.n_colors + 1, sm->s);
+    sm->rast_done.zero(sm->s);
+  }
+  LSB_CUDA(cudaStreamSynchronize(sm->s));
+  return sm.release();
+}
+
+void smoother_apply(const StandaloneSmoother& sm, int mode, const double* r, double* e) {
+  SchwarzView sv = sm.L.schwarz_view();
+  sv.rast_done = sm.rast_done.get();
+  if (mode == 0) {
+    schwarz_ras(sv, r, e, false, sm.s);
+  } else {
+    LSB_CUDA(cudaMemsetAsync(e, 0, sm.n * 8, sm.s));
+    schwarz_rast(sv, sm.L.sm.color_off, r, e, sm.s);
+  }
+}
+
 double operator_complexity(const Hierarchy& h) {  // hierarchy.hpp:257-261
   double total = 0.0;
   for (const Level& L : h.levels) total += static_cast<double>(L.A.nnz);
@@ -495,11 +565,16 @@ SolveWs::SolveWs(const Hierarchy& h) {
   e.resize(nl);
   res.resize(nl);
   rhs.resize(nl);
+  rast_done.resize(nl);
   for (size_t l = 0; l < nl; ++l) {
     const int64_t n = std::max<int64_t>(h.levels[l].A.nr, 1);
     e[l].alloc(n, s);
     res[l].alloc(n, s);
     rhs[l].alloc(n, s);
+    if (h.levels[l].sm.n_groups > 0) {
+      rast_done[l].alloc(h.levels[l].sm.n_colors + 1, s);
+      rast_done[l].zero(s);
+    }
   }
   red.init(s);
   for (auto& e : ev) LSB_CUDA(cudaEventCreate(&e));
@@ -511,6 +586,7 @@ SolveWs::~SolveWs() {
     e.clear();
     res.clear();
     rhs.clear();
+    rast_done.clear();
     red.partial.release();
     red.ticket.release();
     for (auto& e : ev)
@@ -538,7 +614,8 @@ void vcycle(const Hierarchy& h, SolveWs& ws, int64_t level, const double* r, dou
     dense_matvec(h.coarse_inv.get(), h.n_coarse, r, e, s);
     return;
   }
-  const SchwarzView sv = L.schwarz_view();
+  SchwarzView sv = L.schwarz_view();
+  sv.rast_done = ws.rast_done[level].get();  // this call's own counters: concurrent solves share the handle
   double* res = ws.res[level].get();
   if (h.params.pre_sweeps == 0) LSB_CUDA(cudaMemsetAsync(e, 0, n * 8, s));
   for (uint64_t sw = 0; sw < h.params.pre_sweeps; ++sw) {

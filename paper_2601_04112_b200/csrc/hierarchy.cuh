@@ -60,6 +60,20 @@ struct Hierarchy {
   ~Hierarchy();
 };
 
+// build_smoother(a, topo) on a caller matrix and topology (smoother.hpp:38-58)
+// without a hierarchy: the level-0-style Schwarz blocks of one operator.
+struct StandaloneSmoother {
+  Level L;
+  DBuf<int32_t> rast_done;
+  int64_t n = 0;
+  cudaStream_t s = nullptr;
+  ~StandaloneSmoother();
+};
+StandaloneSmoother* make_smoother(const lsamgdd_csr* a, int64_t n_agg, const int64_t* omega_off, const int64_t* omega,
+                                  const int64_t* gamma_off, const int64_t* gamma, const int64_t* colors);
+// apply(smoother, r, mode) (smoother.hpp:65-83), mode 0 RAS / 1 RAS-T; device vectors, on sm.s
+void smoother_apply(const StandaloneSmoother& sm, int mode, const double* r, double* e);
+
 // parameter / input checks of setup (hierarchy.hpp:107-117), host only
 void validate_setup(const lsamgdd_csr* g0, const lsamgdd_params* p);
 
@@ -70,6 +84,7 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* params);
 struct SolveWs {
   cudaStream_t s = nullptr;
   std::vector<DBuf<double>> e, res, rhs;  // per level
+  std::vector<DBuf<int32_t>> rast_done;   // per level: colour completion counters of the one-launch RAS-T
   Reducer red;
   cudaEvent_t ev[6] = {};  // level-0 RAS / RAS-T brackets, then the PCG operator Gᵀ(G p)
   bool timing = false;

@@ -738,6 +738,23 @@ void build_lane_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, con
     sm.lane_ras_items.upload(ri, s);
     sm.lane_rast_items.upload(ti, s);
   }
+  {  // inputs of the persistent TMA-pipelined sweep
+    std::vector<int32_t> gc(sm.n_groups), cg(n_colors + 1, 0);
+    int64_t blk_b = 0, ids_b = 0;
+    for (int64_t c = 0; c < n_colors; ++c) {
+      cg[c] = static_cast<int32_t>(sm.color_goff[c + 1] - sm.color_goff[c]);
+      for (int64_t g = sm.color_goff[c]; g < sm.color_goff[c + 1]; ++g) gc[g] = static_cast<int32_t>(c);
+    }
+    for (int64_t g = 0; g < sm.n_groups; ++g) {
+      blk_b = std::max<int64_t>(blk_b, (g_blk_off[g + 1] - g_blk_off[g]) * 8);
+      ids_b = std::max<int64_t>(ids_b, (g_ids_off[g + 1] - g_ids_off[g]) * 4);
+    }
+    sm.g_color.upload(gc, s);
+    sm.color_groups.upload(cg, s);
+    sm.n_colors = n_colors;
+    sm.stage_blk_bytes = blk_b;
+    sm.stage_ids_bytes = ids_b;
+  }
   DBuf<int32_t> d_agg;
   d_agg.upload(g_agg, s);
   sm.g_nw.upload(g_nw, s);

@@ -50,6 +50,12 @@ struct DevSmoother {
   // warp-per-output-row work items over the groups: (group << 8) | row
   DBuf<int32_t> lane_ras_items, lane_rast_items;
   std::vector<int64_t> lane_rast_color_off;  // host, n_colors + 1
+  // persistent TMA-pipelined sweep over the groups (k_schwarz_tma): per-group colour, groups
+  // per colour (the RAS-T completion counters live in each call's workspace); stage capacity
+  // in bytes of the largest group (0: path not available)
+  DBuf<int32_t> g_color, color_groups;
+  int64_t n_colors = 0;
+  int64_t stage_blk_bytes = 0, stage_ids_bytes = 0;
   // Row layout for large subdomains (warp per output row, many warps per
   // aggregate): per aggregate the full ω×Ω rows of the inverse (F, nω×nΩ)
   // then its Γ columns transposed (Gt, nΓ×nω), so that RAS (rows of F) and

@@ -397,6 +397,301 @@ void schwarz_lrow_launch(const SchwarzView& v, const int32_t* items, int64_t i0,
   LSB_LAUNCH();
 }
 
+// ---- persistent TMA-pipelined sweep over the lane-interleaved groups --------------------
+//
+// One CTA per SM walks the groups g = blockIdx.x, blockIdx.x + gridDim.x, …
+// (the groups are colour-sorted). A producer thread streams each group's
+// contiguous block ([nblk][32] doubles, ~48 KB for 3×3 aggregates with
+// overlap 1) and index list ([nΩ][32] int32) into a ring of shared-memory
+// stages with two 1-D bulk copies (cp.async.bulk, completion on an mbarrier);
+// nine consumer warps gather the group's r values once into shared memory,
+// compute one output row per warp and lane (lane = aggregate of the group)
+// from the staged block and release the stage. HBM sees only long bulk reads;
+// the LSU handles just the r gather and the e scatter.
+// RAS-T (MODE 2) adds into e over the overlapping Ω sets: a group adds only
+// after every group of the earlier colours has added (per-colour completion
+// counters in global memory, reset by the last CTA), which keeps the
+// colour-ordered, deterministic sums of the multi-launch version in one launch
+// while the bulk copies of the next colour's groups keep streaming.
+constexpr int kTmaConsumers = 9;  // consumer warps per team
+constexpr int kTmaTeams = 3;      // consumer teams; team t takes this CTA's groups k ≡ t (mod 3)
+constexpr int kTmaThreads = (kTmaTeams * kTmaConsumers + 1) * 32;  // + one producer warp
+constexpr int kTmaHead = 256;     // barriers and per-stage metadata; then r staging [teams][rs_rows][32], then the stages
+
+// One output row of a group of compile-time shape (NW, NG) from the staged block (blk, rs already
+// offset by the lane): every shared load is issued before the sums; same summation order as the
+// generic loop (even terms into s0, odd into s1).
+template <int MODE, int NW, int NG>
+__device__ __forceinline__ double tma_row_fixed(const double* blk, const double* rs, int row) {
+  constexpr int P0 = NW * (NW + 1) / 2;
+  double s0 = 0.0, s1 = 0.0;
+  if (MODE < 2 || row < NW) {
+    double bv[NW], rv[NW];
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      const int lo = row < j ? row : j, hi = row < j ? j : row;
+      bv[j] = blk[(lo * NW - (lo * (lo - 1)) / 2 + (hi - lo)) * 32];
+      rv[j] = rs[j * 32];
+    }
+#pragma unroll
+    for (int j = 0; j < NW; ++j) {
+      if (j & 1)
+        s1 += bv[j] * rv[j];
+      else
+        s0 += bv[j] * rv[j];
+    }
+    if (MODE < 2) {
+      const double* bg = blk + (P0 + row * NG) * 32;
+      double gv[NG], gr[NG];
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        gv[q] = bg[q * 32];
+        gr[q] = rs[(NW + q) * 32];
+      }
+#pragma unroll
+      for (int q = 0; q < NG; ++q) {
+        if (q & 1)
+          s1 += gv[q] * gr[q];
+        else
+          s0 += gv[q] * gr[q];
+      }
+    }
+  } else {
+    const double* bg = blk + (P0 + (row - NW)) * 32;
+    double bv[NW], rv[NW];
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      bv[i] = bg[i * NG * 32];
+      rv[i] = rs[i * 32];
+    }
+#pragma unroll
+    for (int i = 0; i < NW; ++i) {
+      if (i & 1)
+        s1 += bv[i] * rv[i];
+      else
+        s0 += bv[i] * rv[i];
+    }
+  }
+  return s0 + s1;
+}
+
+__device__ __forceinline__ uint32_t s_u32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void s_mbar_init(uint64_t* bar, int count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void s_mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok)
+                 : "r"(s_u32(bar)), "r"(parity)
+                 : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void s_mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void s_bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(s_u32(dst)),
+               "l"(src), "r"(bytes), "r"(s_u32(bar))
+               : "memory");
+}
+
+// done: the RAS-T completion counters of this call's workspace (n_colors + 1 ints, zero at entry)
+template <int MODE>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    k_schwarz_tma(SchwarzView v, const double* __restrict__ r, double* __restrict__ e, int32_t* done, int n_stage,
+                  int stage_bytes, int blk_cap, int rs_rows) {
+  extern __shared__ __align__(128) unsigned char tma_smem[];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem);  // [8]
+  uint64_t* empty = full + 8;                                // [8]
+  int4* meta = reinterpret_cast<int4*>(tma_smem + 128);      // [8] {nω, nΓ, colour, -}
+  double* rs_all = reinterpret_cast<double*>(tma_smem + kTmaHead);
+  unsigned char* stages = tma_smem + kTmaHead + ((kTmaTeams * rs_rows * 32 * 8 + 127) & ~127);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int k = 0; k < n_stage; ++k) {
+      s_mbar_init(&full[k], 1);
+      s_mbar_init(&empty[k], kTmaConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t ng_total = v.n_groups;
+  if (warp == kTmaTeams * kTmaConsumers) {  // producer
+    if (lane == 0) {
+      int k = 0;
+      for (int64_t g = blockIdx.x; g < ng_total; g += gridDim.x, ++k) {
+        const int st = k % n_stage;
+        const int64_t b0 = v.g_blk_off[g], i0 = v.g_ids_off[g];
+        const uint32_t bb = static_cast<uint32_t>((v.g_blk_off[g + 1] - b0) * 8);
+        const uint32_t ib = static_cast<uint32_t>((v.g_ids_off[g + 1] - i0) * 4);
+        const int4 mt = make_int4(v.g_nw[g], v.g_ng[g], MODE == 2 ? v.g_color[g] : 0, 0);
+        if (k >= n_stage) s_mbar_wait(&empty[st], ((k / n_stage) - 1) & 1);
+        meta[st] = mt;
+        unsigned char* dst = stages + int64_t(st) * stage_bytes;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[st])), "r"(bb + ib)
+                     : "memory");
+        s_bulk_load(dst, v.lane_blk + b0, bb, &full[st]);
+        s_bulk_load(dst + blk_cap, v.lane_ids + i0, ib, &full[st]);
+      }
+    }
+  } else {  // consumer teams
+    const int team = warp / kTmaConsumers, cw = warp % kTmaConsumers;
+    double* rs = rs_all + team * (rs_rows * 32);
+    auto cbar = [team]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "n"(kTmaConsumers * 32) : "memory"); };
+    int verified = 0;  // colours < verified have finished adding (MODE 2)
+    int cur_colour = -1;  // colour of this team's groups whose adds are not signalled yet
+    // colour c is complete once every (CTA, team) pair that owns groups of it has signalled
+    auto signal_colour = [&](int c) {
+      __threadfence();
+      cbar();
+      if (cw == 0 && lane == 0) atomicAdd(&done[c], 1);
+    };
+    int k = team;
+    for (int64_t g = blockIdx.x + int64_t(team) * gridDim.x; g < ng_total; g += int64_t(kTmaTeams) * gridDim.x, k += kTmaTeams) {
+      const int st = k % n_stage;
+      s_mbar_wait(&full[st], (k / n_stage) & 1);
+      const int4 mt = meta[st];
+      const int nw = mt.x, ngm = mt.y, m = nw + ngm, colour = mt.z;
+      const unsigned char* base = stages + int64_t(st) * stage_bytes;
+      const double* blk = reinterpret_cast<const double*>(base) + lane;
+      const int32_t* ids = reinterpret_cast<const int32_t*>(base + blk_cap) + lane;
+      const int nr = MODE < 2 ? m : nw;
+      for (int j = cw; j < nr; j += kTmaConsumers) {
+        const int id = ids[j * 32];
+        rs[j * 32 + lane] = id >= 0 ? __ldcg(&r[id]) : 0.0;
+      }
+      if (MODE == 2) {
+        if (colour != cur_colour) {  // this team leaves a colour: publish its adds
+          if (cur_colour >= 0) signal_colour(cur_colour);
+          cur_colour = colour;
+        }
+        if (cw == 0 && lane == 0) {
+          for (; verified < colour; ++verified) {
+            const int pairs = kTmaTeams * static_cast<int>(gridDim.x);
+            const int want = min(v.color_groups[verified], pairs);
+            while (*reinterpret_cast<volatile int*>(&done[verified]) < want) __nanosleep(64);
+          }
+          __threadfence();
+        }
+        __syncwarp();
+        verified = colour;
+      }
+      cbar();
+      const int p0 = nw * (nw + 1) / 2;
+      const int nout = MODE < 2 ? nw : m;
+      // this warp's rows: cw, cw + 9, … ; their old e values (accumulating modes) are fetched up front
+      constexpr int kMaxRows = (kLaneMaxSub + kTmaConsumers - 1) / kTmaConsumers;
+      double eold[kMaxRows];
+      int outs[kMaxRows];
+#pragma unroll
+      for (int q = 0; q < kMaxRows; ++q) {
+        const int row = cw + q * kTmaConsumers;
+        outs[q] = row < nout ? ids[row * 32] : -1;
+        eold[q] = (MODE != 0 && outs[q] >= 0) ? __ldcg(&e[outs[q]]) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kMaxRows; ++q) {
+        const int row = cw + q * kTmaConsumers;
+        if (row >= nout) break;
+        double s0 = 0.0, s1 = 0.0;
+        if (nw == 9 && ngm == 16) {  // 3×3 aggregates with overlap 1 (config 2 interior)
+          s0 = tma_row_fixed<MODE, 9, 16>(blk, rs + lane, row);
+        } else if (MODE < 2 || row < nw) {  // the ω×ω triangle, then (RAS) the row of the ω×Γ block
+#pragma unroll 3
+          for (int j = 0; j < nw; ++j) {
+            const int lo = row < j ? row : j, hi = row < j ? j : row;
+            const int kk = lo * nw - (lo * (lo - 1)) / 2 + (hi - lo);
+            const double pr = blk[kk * 32] * rs[j * 32 + lane];
+            if (j & 1)
+              s1 += pr;
+            else
+              s0 += pr;
+          }
+          if (MODE < 2) {
+            const double* bg = blk + (p0 + row * ngm) * 32;
+#pragma unroll 4
+            for (int qq = 0; qq < ngm; ++qq) {
+              const double pr = bg[qq * 32] * rs[(nw + qq) * 32 + lane];
+              if (qq & 1)
+                s1 += pr;
+              else
+                s0 += pr;
+            }
+          }
+        } else {  // RAS-T, Γ row: column (row - nω) of the ω×Γ block
+          const double* bg = blk + (p0 + (row - nw)) * 32;
+#pragma unroll 3
+          for (int i = 0; i < nw; ++i) {
+            const double pr = bg[i * ngm * 32] * rs[i * 32 + lane];
+            if (i & 1)
+              s1 += pr;
+            else
+              s0 += pr;
+          }
+        }
+        if (outs[q] >= 0) {
+          const double sum = s0 + s1;
+          if (MODE == 0)
+            e[outs[q]] = sum;
+          else
+            __stcg(&e[outs[q]], eold[q] + sum);
+        }
+      }
+      cbar();  // every row of the group is out; rs and the stage may be reused
+      if (lane == 0) s_mbar_arrive(&empty[st]);
+    }
+    if (MODE == 2 && cur_colour >= 0) signal_colour(cur_colour);
+  }
+  if (MODE == 2) {  // the last CTA to finish clears the counters for the next launch
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      const int fin = atomicAdd(&done[v.n_colors], 1);
+      if (fin == static_cast<int>(gridDim.x) - 1) {
+        for (int c = 0; c <= v.n_colors; ++c) done[c] = 0;
+        __threadfence();
+      }
+    }
+  }
+}
+
+// true when the launch ran (lane layout present and at least two stages fit)
+template <int MODE>
+bool schwarz_tma_launch(const SchwarzView& v, const double* r, double* e, cudaStream_t s) {
+  if (v.n_groups == 0 || v.stage_blk_bytes == 0) return false;
+  if (MODE == 2 && !v.rast_done) return false;
+  const int blk_cap = static_cast<int>((v.stage_blk_bytes + 127) & ~int64_t(127));
+  const int stage_bytes = blk_cap + static_cast<int>((v.stage_ids_bytes + 127) & ~int64_t(127));
+  const int rs_rows = static_cast<int>(v.max_sub);
+  const int fixed = kTmaHead + ((kTmaTeams * rs_rows * 32 * 8 + 127) & ~127);
+  constexpr int kMaxSmem = 226 * 1024;  // 227 KB per CTA minus the kernel's static 1 KB
+  const int budget = kMaxSmem - fixed;
+  const int n_stage = std::min(8, budget / stage_bytes);
+  if (n_stage < 2 || rs_rows > kLaneMaxSub) return false;
+  const size_t smem = size_t(fixed) + size_t(n_stage) * stage_bytes;
+  static std::atomic<uint64_t> attr{0};
+  if (first_on_device(attr))
+    LSB_CUDA(cudaFuncSetAttribute(k_schwarz_tma<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxSmem));
+  const int grid = static_cast<int>(std::min<int64_t>(v.n_groups, sm_count()));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(kTmaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  LSB_CUDA(cudaLaunchKernelEx(&cfg, k_schwarz_tma<MODE>, v, r, e, v.rast_done, n_stage, stage_bytes, blk_cap, rs_rows));
+  LSB_LAUNCH();
+  return true;
+}
+
 // Row layout (large subdomains): one warp per output row, lanes over a
 // contiguous row of the explicit inverse, fixed xor-tree reduction (the
 // result is deterministic). RAS (MODE 0/1): row i of F · r[Ω] -> e[ω_i];
@@ -867,10 +1162,13 @@ void schwarz_ras(const SchwarzView& v, const double* r, double* e, bool accumula
     return;
   }
   if (v.n_groups > 0) {
-    if (accumulate)
+    if (accumulate) {
+      if (schwarz_tma_launch<1>(v, r, e, s)) return;
       schwarz_lrow_launch<1>(v, v.lane_ras_items, 0, v.n_lane_ras_items, r, e, s);
-    else
+    } else {
+      if (schwarz_tma_launch<0>(v, r, e, s)) return;
       schwarz_lrow_launch<0>(v, v.lane_ras_items, 0, v.n_lane_ras_items, r, e, s);
+    }
     return;
   }
   if (accumulate)
@@ -887,6 +1185,7 @@ void schwarz_rast(const SchwarzView& v, const std::vector<int64_t>& color_off, c
     return;
   }
   if (v.n_groups > 0) {
+    if (schwarz_tma_launch<2>(v, r, e, s)) return;
     const auto& co = *v.lane_rast_color_off;
     for (size_t c = 0; c + 1 < co.size(); ++c) schwarz_lrow_launch<2>(v, v.lane_rast_items, co[c], co[c + 1], r, e, s);
     return;

@@ -31,6 +31,12 @@ struct SchwarzView {
   int64_t n_lane_ras_items;
   const int32_t* lane_rast_items;
   const std::vector<int64_t>* lane_rast_color_off;
+  // persistent TMA-pipelined sweep (k_schwarz_tma)
+  const int32_t* g_color;
+  const int32_t* color_groups;
+  int32_t* rast_done;
+  int n_colors;
+  int64_t stage_blk_bytes, stage_ids_bytes;
   // row layout (large subdomains), see DevSmoother
   bool rows;
   const int64_t* row_off;

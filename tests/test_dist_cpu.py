@@ -35,7 +35,7 @@ def test_reference_arm_rank0_only():
     env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29733", os.path.join(ROOT, "bench.py"),
-           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3", "--sample-grid", "16"]
+           "--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "3", "--grid", "32"]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=ROOT)
     assert res.returncode == 0, res.stdout[-2000:] + res.stderr[-2000:]
     lines = [l for l in res.stdout.splitlines() if l.startswith("{")]

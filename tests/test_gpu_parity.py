@@ -356,6 +356,19 @@ def test_cpp_shim_drop_in(gpu):
     assert res.returncode == 0, res.stdout + res.stderr
 
 
+def test_cpp_shim_acceptance(gpu):
+    """acceptance.cpp's solve_system and checks 2, 3, 4, 11 plus the spectra_csv
+    dump, compiled against the shim with the hot-path calls taken from
+    lsamgdd::b200 (tests/cpp/shim_acceptance.cpp)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(__file__), "cpp", "shim_acceptance.bin")
+    if not os.path.exists(exe):
+        pytest.skip("shim_acceptance.bin not built (needs /root/reference at build time)")
+    res = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stdout + res.stderr
+
+
 def _fixture(name):
     import json
     import os
