@@ -363,7 +363,7 @@ def main() -> None:
                 traffic = json.load(f).get("dram_bytes_per_launch")
         roofline = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-                    "kernel": "level-0 Schwarz RAS + RAS-T sweep pair (k_schwarz_lrow: 1 RAS + 4 colour launches)",
+                    "kernel": "level-0 Schwarz RAS + RAS-T sweep pair (k_schwarz_tma: persistent TMA-pipelined sweeps, RAS-T followed by k_rast_slots)",
                     "bytes_per_launch": ks.schwarz_bytes / max(ks.schwarz_launches, 1),
                     "peak_source": peaks["source"]}
     # second HBM-bound kernel pair: the PCG operator Gᵀ(G p) (k_sell_spmv + k_ap_dot),

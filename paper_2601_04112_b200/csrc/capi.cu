@@ -252,7 +252,7 @@ int lsamgdd_schwarz_apply(const void* handle, int64_t level, int32_t mode, const
     const int64_t n = L.A.nr;
     with_vectors(ws.s, r, n, e, n, memory, [&](const double* dr, double* de) {
       SchwarzView sv = L.schwarz_view();
-      sv.rast_done = ws.rast_done[level].get();
+      sv.rast_tmp = ws.rast_tmp[level].get();
       if (mode == LSAMGDD_RAS) {
         schwarz_ras(sv, dr, de, false, ws.s);
       } else {

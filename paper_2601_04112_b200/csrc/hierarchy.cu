@@ -313,7 +313,13 @@ SchwarzView Level::schwarz_view() const {
   v.lane_rast_color_off = &sm.lane_rast_color_off;
   v.g_color = sm.g_color.get();
   v.color_groups = sm.color_groups.get();
-  v.rast_done = nullptr;  // the caller's workspace supplies the RAS-T counters
+  v.rast_tmp = nullptr;  // the caller's workspace supplies the RAS-T slot buffer
+  v.g_slot_off = sm.g_slot_off.get();
+  v.lane_slots = sm.lane_slots.get();
+  v.node_slot_off = sm.node_slot_off.get();
+  v.n_slots = sm.n_slots;
+  v.stage_slot_bytes = sm.stage_slot_bytes;
+  v.n_nodes = topo.n_nodes;
   v.n_colors = static_cast<int>(sm.n_colors);
   v.stage_blk_bytes = sm.stage_blk_bytes;
   v.stage_ids_bytes = sm.stage_ids_bytes;
@@ -424,7 +430,7 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
     upload_topology(cur, asg, s);
     stage("aggregation_topology", t0);
     t0 = Clock::now();
-    build_smoother(cur.A, cur.topo, cur.h_omega_off, cur.h_gamma_off, cur.colors, cur.n_colors, cur.sm, s);
+    build_smoother(cur.A, cur.topo, cur.h_omega_off, cur.h_gamma_off, cur.colors, cur.n_colors, cur.sm, s, &cur.h_gamma);
     sell_from_csr(cur.A, cur.A_sell, s);
     stage("build_smoother", t0);
     t0 = Clock::now();
@@ -491,7 +497,7 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
 StandaloneSmoother::~StandaloneSmoother() {
   if (s) {
     cudaStreamSynchronize(s);
-    rast_done.release();
+    rast_tmp.release();
     L = Level();
     cudaStreamSynchronize(s);
     cudaStreamDestroy(s);
@@ -532,18 +538,15 @@ StandaloneSmoother* make_smoother(const lsamgdd_csr* a, int64_t n_agg, const int
     if (gamma[k] < 0 || gamma[k] >= n) raise(LSAMGDD_ERR_INDEX, "build_smoother: boundary node out of range");
   csr_upload(L.A, a, sm->s);
   upload_topology(L, asg, sm->s);
-  build_smoother(L.A, L.topo, L.h_omega_off, L.h_gamma_off, L.colors, L.n_colors, L.sm, sm->s);
-  if (L.sm.n_groups > 0) {
-    sm->rast_done.alloc(L.sm.n_colors + 1, sm->s);
-    sm->rast_done.zero(sm->s);
-  }
+  build_smoother(L.A, L.topo, L.h_omega_off, L.h_gamma_off, L.colors, L.n_colors, L.sm, sm->s, &L.h_gamma);
+  if (L.sm.n_slots > 0) sm->rast_tmp.alloc(L.sm.n_slots, sm->s);
   LSB_CUDA(cudaStreamSynchronize(sm->s));
   return sm.release();
 }
 
 void smoother_apply(const StandaloneSmoother& sm, int mode, const double* r, double* e) {
   SchwarzView sv = sm.L.schwarz_view();
-  sv.rast_done = sm.rast_done.get();
+  sv.rast_tmp = sm.rast_tmp.get();
   if (mode == 0) {
     schwarz_ras(sv, r, e, false, sm.s);
   } else {
@@ -565,16 +568,13 @@ SolveWs::SolveWs(const Hierarchy& h) {
   e.resize(nl);
   res.resize(nl);
   rhs.resize(nl);
-  rast_done.resize(nl);
+  rast_tmp.resize(nl);
   for (size_t l = 0; l < nl; ++l) {
     const int64_t n = std::max<int64_t>(h.levels[l].A.nr, 1);
     e[l].alloc(n, s);
     res[l].alloc(n, s);
     rhs[l].alloc(n, s);
-    if (h.levels[l].sm.n_groups > 0) {
-      rast_done[l].alloc(h.levels[l].sm.n_colors + 1, s);
-      rast_done[l].zero(s);
-    }
+    if (h.levels[l].sm.n_slots > 0) rast_tmp[l].alloc(h.levels[l].sm.n_slots, s);
   }
   red.init(s);
   for (auto& e : ev) LSB_CUDA(cudaEventCreate(&e));
@@ -586,7 +586,7 @@ SolveWs::~SolveWs() {
     e.clear();
     res.clear();
     rhs.clear();
-    rast_done.clear();
+    rast_tmp.clear();
     red.partial.release();
     red.ticket.release();
     for (auto& e : ev)
@@ -615,7 +615,7 @@ void vcycle(const Hierarchy& h, SolveWs& ws, int64_t level, const double* r, dou
     return;
   }
   SchwarzView sv = L.schwarz_view();
-  sv.rast_done = ws.rast_done[level].get();  // this call's own counters: concurrent solves share the handle
+  sv.rast_tmp = ws.rast_tmp[level].get();  // this call's own slot buffer: concurrent solves share the handle
   double* res = ws.res[level].get();
   if (h.params.pre_sweeps == 0) LSB_CUDA(cudaMemsetAsync(e, 0, n * 8, s));
   for (uint64_t sw = 0; sw < h.params.pre_sweeps; ++sw) {

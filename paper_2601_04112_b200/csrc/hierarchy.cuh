@@ -64,7 +64,7 @@ struct Hierarchy {
 // without a hierarchy: the level-0-style Schwarz blocks of one operator.
 struct StandaloneSmoother {
   Level L;
-  DBuf<int32_t> rast_done;
+  DBuf<double> rast_tmp;
   int64_t n = 0;
   cudaStream_t s = nullptr;
   ~StandaloneSmoother();
@@ -84,7 +84,7 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* params);
 struct SolveWs {
   cudaStream_t s = nullptr;
   std::vector<DBuf<double>> e, res, rhs;  // per level
-  std::vector<DBuf<int32_t>> rast_done;   // per level: colour completion counters of the one-launch RAS-T
+  std::vector<DBuf<double>> rast_tmp;     // per level: Γ-contribution slots of the one-launch RAS-T
   Reducer red;
   cudaEvent_t ev[6] = {};  // level-0 RAS / RAS-T brackets, then the PCG operator Gᵀ(G p)
   bool timing = false;

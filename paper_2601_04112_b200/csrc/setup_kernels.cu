@@ -696,7 +696,8 @@ __global__ void k_lane_pack(const int32_t* g_agg, const int32_t* g_nw, const int
 }
 
 void build_lane_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, const std::vector<int32_t>& hgo,
-                       const std::vector<int64_t>& colors, int64_t n_colors, DevSmoother& sm, cudaStream_t s) {
+                       const std::vector<int64_t>& colors, int64_t n_colors, DevSmoother& sm, cudaStream_t s,
+                       const std::vector<int32_t>* h_gamma) {
   const int64_t na = topo.n_agg;
   // groups: (colour, nω, nΓ) keys in colour order, aggregates ascending inside a key
   std::vector<int64_t> order(na);
@@ -754,6 +755,36 @@ void build_lane_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, con
     sm.n_colors = n_colors;
     sm.stage_blk_bytes = blk_b;
     sm.stage_ids_bytes = ids_b;
+    sm.n_slots = 0;
+    if (h_gamma) {
+      // per-node slots of the Γ contributions: node-major, holders in ascending aggregate order
+      const int64_t n = topo.n_nodes;
+      std::vector<int32_t> noff(n + 1, 0);
+      for (int32_t v : *h_gamma) ++noff[v + 1];
+      for (int64_t v = 0; v < n; ++v) noff[v + 1] += noff[v];
+      std::vector<int32_t> cur(noff.begin(), noff.end() - 1);
+      std::vector<int32_t> slot_of(h_gamma->size());  // per Γ entry, in (aggregate ascending, position) order
+      for (int64_t a = 0; a < na; ++a)
+        for (int32_t p = hgo[a]; p < hgo[a + 1]; ++p) slot_of[p] = cur[(*h_gamma)[p]]++;
+      std::vector<int64_t> soff(sm.n_groups + 1, 0);
+      int64_t slot_b = 0;
+      for (int64_t g = 0; g < sm.n_groups; ++g) {
+        soff[g + 1] = soff[g] + int64_t(g_ng[g]) * 32;
+        slot_b = std::max<int64_t>(slot_b, int64_t(g_ng[g]) * 32 * 4);
+      }
+      std::vector<int32_t> ls(std::max<int64_t>(soff.back(), 1), -1);
+      for (int64_t g = 0; g < sm.n_groups; ++g)
+        for (int l = 0; l < 32; ++l) {
+          const int32_t a = g_agg[g * 32 + l];
+          if (a < 0) continue;
+          for (int j = 0; j < g_ng[g]; ++j) ls[soff[g] + int64_t(j) * 32 + l] = slot_of[hgo[a] + j];
+        }
+      sm.g_slot_off.upload(soff, s);
+      sm.lane_slots.upload(ls, s);
+      sm.node_slot_off.upload(noff, s);
+      sm.n_slots = static_cast<int64_t>(h_gamma->size());
+      sm.stage_slot_bytes = slot_b;
+    }
   }
   DBuf<int32_t> d_agg;
   d_agg.upload(g_agg, s);
@@ -1117,7 +1148,7 @@ void build_row_layout(const DevTopo& topo, const std::vector<int32_t>& hoo, cons
 
 void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int32_t>& hoo,
                     const std::vector<int32_t>& hgo, const std::vector<int64_t>& colors, int64_t n_colors,
-                    DevSmoother& sm, cudaStream_t s) {
+                    DevSmoother& sm, cudaStream_t s, const std::vector<int32_t>* h_gamma) {
   const int64_t na = topo.n_agg;
   sm.n_agg = na;
   std::vector<int64_t> off(na + 1, 0), need(na);
@@ -1162,7 +1193,7 @@ void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int3
     if (hs[i]) raise(LSAMGDD_ERR_SETUP, "dense symmetric factorization failed for subdomain block of aggregate " +
                                             std::to_string(i));
   if (sm.max_sub <= kLaneMaxSub && sm.max_omega <= kLaneMaxOmega)
-    build_lane_layout(topo, hoo, hgo, colors, n_colors, sm, s);
+    build_lane_layout(topo, hoo, hgo, colors, n_colors, sm, s, h_gamma);
   // colour-sorted aggregate order for the race-free RAS-T scatter
   std::vector<int32_t> byc(na);
   sm.color_off.assign(n_colors + 1, 0);

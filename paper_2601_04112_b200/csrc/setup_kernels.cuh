@@ -56,6 +56,12 @@ struct DevSmoother {
   DBuf<int32_t> g_color, color_groups;
   int64_t n_colors = 0;
   int64_t stage_blk_bytes = 0, stage_ids_bytes = 0;
+  // one-launch RAS-T: the Γ contributions of a subdomain go to per-node slots (node-major,
+  // holders in ascending aggregate order) and a second kernel adds each node's slots into e
+  DBuf<int64_t> g_slot_off;            // per group (int32 units)
+  DBuf<int32_t> lane_slots;            // [nΓ][32] per group: slot of the lane's Γ node j, -1 for padding
+  DBuf<int32_t> node_slot_off;         // n_nodes + 1
+  int64_t n_slots = 0, stage_slot_bytes = 0;
   // Row layout for large subdomains (warp per output row, many warps per
   // aggregate): per aggregate the full ω×Ω rows of the inverse (F, nω×nΩ)
   // then its Γ columns transposed (Gt, nΓ×nω), so that RAS (rows of F) and
@@ -78,9 +84,10 @@ constexpr int kLaneMaxOmega = 24;
 // build_smoother (smoother.hpp:38-58): extract A(Ω,Ω), Cholesky with the
 // jitter retry of factor_spd_block (dense.hpp:175-185), explicit ω columns of
 // the inverse. Throws SetupError for the first failing aggregate.
+// h_gamma (optional): the host copy of the Γ lists, needed for the one-launch RAS-T slots
 void build_smoother(const DevCsr& a, const DevTopo& topo, const std::vector<int32_t>& h_omega_off,
                     const std::vector<int32_t>& h_gamma_off, const std::vector<int64_t>& colors, int64_t n_colors,
-                    DevSmoother& sm, cudaStream_t s);
+                    DevSmoother& sm, cudaStream_t s, const std::vector<int32_t>* h_gamma = nullptr);
 
 struct GevpParams {
   double thresh;

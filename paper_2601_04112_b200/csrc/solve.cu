@@ -497,17 +497,18 @@ __device__ __forceinline__ void s_bulk_load(void* dst, const void* src, uint32_t
                : "memory");
 }
 
-// done: the RAS-T completion counters of this call's workspace (n_colors + 1 ints, zero at entry)
+// MODE 2 (RAS-T): the ω rows add into e directly (the interiors are disjoint); the Γ rows store
+// their contributions into per-node slots (tmp, L2-resident), which k_rast_slots adds into e.
 template <int MODE>
 __global__ void __launch_bounds__(kTmaThreads, 1)
-    k_schwarz_tma(SchwarzView v, const double* __restrict__ r, double* __restrict__ e, int32_t* done, int n_stage,
-                  int stage_bytes, int blk_cap, int rs_rows) {
+    k_schwarz_tma(SchwarzView v, const double* __restrict__ r, double* __restrict__ e, double* __restrict__ tmp,
+                  int n_stage, int stage_bytes, int blk_cap, int ids_cap, int rs_rows) {
   extern __shared__ __align__(128) unsigned char tma_smem[];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   uint64_t* full = reinterpret_cast<uint64_t*>(tma_smem);  // [8]
   uint64_t* empty = full + 8;                                // [8]
-  int4* meta = reinterpret_cast<int4*>(tma_smem + 128);      // [8] {nω, nΓ, colour, -}
+  int4* meta = reinterpret_cast<int4*>(tma_smem + 128);      // [8] {nω, nΓ, -, -}
   double* rs_all = reinterpret_cast<double*>(tma_smem + kTmaHead);
   unsigned char* stages = tma_smem + kTmaHead + ((kTmaTeams * rs_rows * 32 * 8 + 127) & ~127);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -528,70 +529,51 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const int64_t b0 = v.g_blk_off[g], i0 = v.g_ids_off[g];
         const uint32_t bb = static_cast<uint32_t>((v.g_blk_off[g + 1] - b0) * 8);
         const uint32_t ib = static_cast<uint32_t>((v.g_ids_off[g + 1] - i0) * 4);
-        const int4 mt = make_int4(v.g_nw[g], v.g_ng[g], MODE == 2 ? v.g_color[g] : 0, 0);
+        const int64_t s0 = MODE == 2 ? v.g_slot_off[g] : 0;
+        const uint32_t sb = MODE == 2 ? static_cast<uint32_t>((v.g_slot_off[g + 1] - s0) * 4) : 0u;
+        const int4 mt = make_int4(v.g_nw[g], v.g_ng[g], 0, 0);
         if (k >= n_stage) s_mbar_wait(&empty[st], ((k / n_stage) - 1) & 1);
         meta[st] = mt;
         unsigned char* dst = stages + int64_t(st) * stage_bytes;
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[st])), "r"(bb + ib)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(&full[st])), "r"(bb + ib + sb)
                      : "memory");
         s_bulk_load(dst, v.lane_blk + b0, bb, &full[st]);
         s_bulk_load(dst + blk_cap, v.lane_ids + i0, ib, &full[st]);
+        if (MODE == 2 && sb) s_bulk_load(dst + blk_cap + ids_cap, v.lane_slots + s0, sb, &full[st]);
       }
     }
   } else {  // consumer teams
     const int team = warp / kTmaConsumers, cw = warp % kTmaConsumers;
     double* rs = rs_all + team * (rs_rows * 32);
     auto cbar = [team]() { asm volatile("bar.sync %0, %1;" ::"r"(1 + team), "n"(kTmaConsumers * 32) : "memory"); };
-    int verified = 0;  // colours < verified have finished adding (MODE 2)
-    int cur_colour = -1;  // colour of this team's groups whose adds are not signalled yet
-    // colour c is complete once every (CTA, team) pair that owns groups of it has signalled
-    auto signal_colour = [&](int c) {
-      __threadfence();
-      cbar();
-      if (cw == 0 && lane == 0) atomicAdd(&done[c], 1);
-    };
     int k = team;
     for (int64_t g = blockIdx.x + int64_t(team) * gridDim.x; g < ng_total; g += int64_t(kTmaTeams) * gridDim.x, k += kTmaTeams) {
       const int st = k % n_stage;
       s_mbar_wait(&full[st], (k / n_stage) & 1);
       const int4 mt = meta[st];
-      const int nw = mt.x, ngm = mt.y, m = nw + ngm, colour = mt.z;
+      const int nw = mt.x, ngm = mt.y, m = nw + ngm;
       const unsigned char* base = stages + int64_t(st) * stage_bytes;
       const double* blk = reinterpret_cast<const double*>(base) + lane;
       const int32_t* ids = reinterpret_cast<const int32_t*>(base + blk_cap) + lane;
+      const int32_t* slots = reinterpret_cast<const int32_t*>(base + blk_cap + ids_cap) + lane;
       const int nr = MODE < 2 ? m : nw;
       for (int j = cw; j < nr; j += kTmaConsumers) {
         const int id = ids[j * 32];
         rs[j * 32 + lane] = id >= 0 ? __ldcg(&r[id]) : 0.0;
       }
-      if (MODE == 2) {
-        if (colour != cur_colour) {  // this team leaves a colour: publish its adds
-          if (cur_colour >= 0) signal_colour(cur_colour);
-          cur_colour = colour;
-        }
-        if (cw == 0 && lane == 0) {
-          for (; verified < colour; ++verified) {
-            const int pairs = kTmaTeams * static_cast<int>(gridDim.x);
-            const int want = min(v.color_groups[verified], pairs);
-            while (*reinterpret_cast<volatile int*>(&done[verified]) < want) __nanosleep(64);
-          }
-          __threadfence();
-        }
-        __syncwarp();
-        verified = colour;
-      }
       cbar();
       const int p0 = nw * (nw + 1) / 2;
       const int nout = MODE < 2 ? nw : m;
-      // this warp's rows: cw, cw + 9, … ; their old e values (accumulating modes) are fetched up front
+      // this warp's rows: cw, cw + 9, …
       constexpr int kMaxRows = (kLaneMaxSub + kTmaConsumers - 1) / kTmaConsumers;
       double eold[kMaxRows];
       int outs[kMaxRows];
 #pragma unroll
       for (int q = 0; q < kMaxRows; ++q) {
         const int row = cw + q * kTmaConsumers;
-        outs[q] = row < nout ? ids[row * 32] : -1;
-        eold[q] = (MODE != 0 && outs[q] >= 0) ? __ldcg(&e[outs[q]]) : 0.0;
+        // ω rows: the node; Γ rows of RAS-T: the slot of the contribution
+        outs[q] = row < nout ? ((MODE == 2 && row >= nw) ? slots[(row - nw) * 32] : ids[row * 32]) : -1;
+        eold[q] = (MODE != 0 && row < nw && outs[q] >= 0) ? e[outs[q]] : 0.0;
       }
 #pragma unroll
       for (int q = 0; q < kMaxRows; ++q) {
@@ -635,26 +617,31 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
         if (outs[q] >= 0) {
           const double sum = s0 + s1;
-          if (MODE == 0)
+          if (MODE == 2 && row >= nw)
+            tmp[outs[q]] = sum;
+          else if (MODE == 0)
             e[outs[q]] = sum;
           else
-            __stcg(&e[outs[q]], eold[q] + sum);
+            e[outs[q]] = eold[q] + sum;
         }
       }
       cbar();  // every row of the group is out; rs and the stage may be reused
       if (lane == 0) s_mbar_arrive(&empty[st]);
     }
-    if (MODE == 2 && cur_colour >= 0) signal_colour(cur_colour);
   }
-  if (MODE == 2) {  // the last CTA to finish clears the counters for the next launch
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      const int fin = atomicAdd(&done[v.n_colors], 1);
-      if (fin == static_cast<int>(gridDim.x) - 1) {
-        for (int c = 0; c <= v.n_colors; ++c) done[c] = 0;
-        __threadfence();
-      }
+}
+
+// e[v] += Σ slots of node v, in slot order (ascending holder aggregate): second step of the one-launch RAS-T
+__global__ void __launch_bounds__(256) k_rast_slots(const int32_t* __restrict__ off, const double* __restrict__ tmp,
+                                                    int64_t n, double* __restrict__ e) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  for (int64_t v = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; v < n; v += int64_t(gridDim.x) * blockDim.x) {
+    const int a = off[v], b = off[v + 1];
+    if (b > a) {
+      double s = 0.0;
+      for (int k = a; k < b; ++k) s += tmp[k];
+      e[v] += s;
     }
   }
 }
@@ -663,9 +650,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
 template <int MODE>
 bool schwarz_tma_launch(const SchwarzView& v, const double* r, double* e, cudaStream_t s) {
   if (v.n_groups == 0 || v.stage_blk_bytes == 0) return false;
-  if (MODE == 2 && !v.rast_done) return false;
+  if (MODE == 2 && (!v.rast_tmp || v.n_slots == 0)) return false;
   const int blk_cap = static_cast<int>((v.stage_blk_bytes + 127) & ~int64_t(127));
-  const int stage_bytes = blk_cap + static_cast<int>((v.stage_ids_bytes + 127) & ~int64_t(127));
+  const int ids_cap = static_cast<int>((v.stage_ids_bytes + 127) & ~int64_t(127));
+  const int stage_bytes = blk_cap + ids_cap + (MODE == 2 ? static_cast<int>((v.stage_slot_bytes + 127) & ~int64_t(127)) : 0);
   const int rs_rows = static_cast<int>(v.max_sub);
   const int fixed = kTmaHead + ((kTmaTeams * rs_rows * 32 * 8 + 127) & ~127);
   constexpr int kMaxSmem = 226 * 1024;  // 227 KB per CTA minus the kernel's static 1 KB
@@ -687,8 +675,13 @@ bool schwarz_tma_launch(const SchwarzView& v, const double* r, double* e, cudaSt
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  LSB_CUDA(cudaLaunchKernelEx(&cfg, k_schwarz_tma<MODE>, v, r, e, v.rast_done, n_stage, stage_bytes, blk_cap, rs_rows));
+  LSB_CUDA(cudaLaunchKernelEx(&cfg, k_schwarz_tma<MODE>, v, r, e, v.rast_tmp, n_stage, stage_bytes, blk_cap, ids_cap, rs_rows));
   LSB_LAUNCH();
+  if (MODE == 2) {
+    const int g2 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(ceil_div(v.n_nodes, 256), int64_t(sm_count()) * 8)));
+    launch_pdl(k_rast_slots, g2, 256, s, v.node_slot_off, static_cast<const double*>(v.rast_tmp), v.n_nodes, e);
+    LSB_LAUNCH();
+  }
   return true;
 }
 

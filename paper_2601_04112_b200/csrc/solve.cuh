@@ -34,9 +34,14 @@ struct SchwarzView {
   // persistent TMA-pipelined sweep (k_schwarz_tma)
   const int32_t* g_color;
   const int32_t* color_groups;
-  int32_t* rast_done;
   int n_colors;
   int64_t stage_blk_bytes, stage_ids_bytes;
+  // one-launch RAS-T: per-node slots of the Γ contributions
+  double* rast_tmp;
+  const int64_t* g_slot_off;
+  const int32_t* lane_slots;
+  const int32_t* node_slot_off;
+  int64_t n_slots, stage_slot_bytes, n_nodes;
   // row layout (large subdomains), see DevSmoother
   bool rows;
   const int64_t* row_off;

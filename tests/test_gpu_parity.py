@@ -66,6 +66,10 @@ CASES = [
     ("c4", 48, {}),
     ("c4", 30, {"eps_perp": 1e-3}),
     ("c4", 30, {"eps_perp": 1e-9}),
+    # config 3 at 128² with the threshold chosen for its runs (the literal 1/0.05 = 20 makes
+    # the reference's own cycle indefinite, test_indefinite_parity), config 5 (3-D, 4³ blocks, 3 levels)
+    ("c3", 128, {"thresh_override": 10.0}),
+    ("c5", 12, {}),
 ]
 
 
@@ -105,7 +109,11 @@ def test_vcycle_and_pcg(gpu, built, name, scale, over):
     cfg, h, ho = built[_key(name, scale, over)]
     r = cfg.rhs
     e, eo = lsamgdd.vcycle(h, r), ho.vcycle(r)
-    assert np.linalg.norm(e - eo) <= VCYCLE_RTOL * np.linalg.norm(eo)
+    # config 5 (max_levels = 3) ends on a dense coarsest level of several hundred unknowns: its explicit
+    # inverse and the oracle's triangular solves differ by cond·eps there (measured 1.7e-10 at 12³; the
+    # Schwarz applies agree to 4e-12, the PCG iterates to 3e-16)
+    rtol = 1e-9 if name == "c5" else VCYCLE_RTOL
+    assert np.linalg.norm(e - eo) <= rtol * np.linalg.norm(eo)
     x, rep = lsamgdd.pcg(h, r, 1e-8, 1000)
     xo, repo = ho.pcg(r, 1e-8, 1000)
     assert rep.converged and repo["converged"]
@@ -367,6 +375,30 @@ def test_cpp_shim_acceptance(gpu):
         pytest.skip("shim_acceptance.bin not built (needs /root/reference at build time)")
     res = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert res.returncode == 0, res.stdout + res.stderr
+
+
+@pytest.mark.parametrize("name,grid", [("c5", 16)])
+def test_hierarchy_matches_golden_fixture(gpu, name, grid):
+    """Whole-hierarchy parity where the CPU run is too slow for the suite (C5 at 16³: 288 s on one
+    core): every level's exports against the hashes the pinned oracle produced
+    (scripts/make_hierarchy_fixture.py), PCG iterations within ±1, solution within 1e-8."""
+    import os
+    from . import _hashes
+    fx = _fixture(f"hier_{name}_{grid}.json")
+    cfg = configs.config(name, grid)
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg, keep_spectra=True))
+    assert h.num_levels == fx["num_levels"]
+    for level, stages in enumerate(fx["levels"]):
+        for stage, ref in stages.items():
+            sizes, arrays = _hashes.gpu_stage(h, level, stage)
+            assert sizes == ref["sizes"], (level, stage)
+            assert _hashes.digest(arrays) == ref["sha256"], (level, stage)
+    assert lsamgdd.operator_complexity(h) == fx["operator_complexity"]
+    x, rep = lsamgdd.pcg(h, cfg.rhs, 1e-8, 1000)
+    assert rep.converged and abs(int(rep.iterations) - fx["pcg_iterations"]) <= 1
+    assert rep.residual_history[-1] <= 1e-8 * rep.residual_history[0]
+    xo = np.load(os.path.join(os.path.dirname(__file__), "golden", f"hier_{name}_{grid}_x.npy"))
+    assert np.linalg.norm(x - xo) <= 1e-8 * np.linalg.norm(xo)
 
 
 def _fixture(name):
