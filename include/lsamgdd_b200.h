@@ -100,7 +100,10 @@ typedef struct lsamgdd_params {
                                   size): build k levels with interpolation and the operators of level k, then stop
                                   without factoring the coarsest level. Such a handle serves exports, level_spmv and
                                   schwarz_apply on levels < k; vcycle and pcg fail with InputError. */
-  uint64_t reserved[3];
+  uint64_t level_offset;       /* 0: the factor is level 0. k > 0 (distributed setup): the factor is level k of a
+                                  hierarchy whose finer levels were built elsewhere — ratios, caps and max_levels
+                                  count from level k, the level-0 hooks do not apply */
+  uint64_t reserved[2];
 } lsamgdd_params;
 
 /* LevelSummary (hierarchy.hpp:32-41). */
@@ -205,6 +208,12 @@ int lsamgdd_build_smoother(const lsamgdd_csr* a, int64_t n_aggregates, const int
 int lsamgdd_smoother_apply(const void* smoother, int32_t mode, const double* r, double* e,
                            int32_t memory, char* err, size_t errlen);
 int lsamgdd_smoother_destroy(void* smoother);
+/* A caller matrix kept on the device for repeated products (the distributed
+ * solve's strip operators): y = m x or y = mᵀ x (the transposed operator is
+ * built on first use), same kernels and summation order as lsamgdd_spmv. */
+int lsamgdd_matrix_create(const lsamgdd_csr* a, void** out_matrix, char* err, size_t errlen);
+int lsamgdd_matrix_spmv(void* matrix, int32_t transpose, const double* x, double* y, int32_t memory,
+                        char* err, size_t errlen);
 /* Host copy of a device matrix: sizes {rows, cols, nnz}; NULL arrays to query. */
 int lsamgdd_matrix_export(const void* matrix, int64_t sizes[3], int64_t* offsets, int64_t* cols,
                           double* vals);

@@ -63,7 +63,8 @@ class Params(C.Structure):
         ("thresh_override", C.c_double),
         ("level0_max_modes", C.c_uint64),
         ("probe_levels", C.c_uint64),
-        ("reserved", C.c_uint64 * 3),
+        ("level_offset", C.c_uint64),
+        ("reserved", C.c_uint64 * 2),
     ]
 
 
@@ -130,6 +131,7 @@ def default_params(**over) -> Params:
     p.thresh_override = 0.0
     p.level0_max_modes = 0
     p.probe_levels = 0
+    p.level_offset = 0
     for k, v in over.items():
         if k == "coarsening_ratios":
             p.n_ratios = len(v)

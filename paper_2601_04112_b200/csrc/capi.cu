@@ -5,6 +5,7 @@
 #include <cstring>
 #include <limits>
 #include <memory>
+#include <mutex>
 #include <new>
 #include <random>
 
@@ -336,10 +337,15 @@ struct OwnStream {
 };
 struct MatrixHandle {
   DevCsr m;
+  Sell sell, sell_t;  // SpMV forms, built on first use
+  bool has_sell = false, has_sell_t = false;
+  std::mutex mu;
   cudaStream_t s = nullptr;
   ~MatrixHandle() {
     if (s) {
       cudaStreamSynchronize(s);
+      sell = Sell();
+      sell_t = Sell();
       m = DevCsr();
       cudaStreamSynchronize(s);
       cudaStreamDestroy(s);
@@ -442,6 +448,43 @@ int lsamgdd_smoother_apply(const void* smoother, int32_t mode, const double* r, 
 int lsamgdd_smoother_destroy(void* smoother) {
   delete static_cast<StandaloneSmoother*>(smoother);
   return LSAMGDD_OK;
+}
+
+int lsamgdd_matrix_create(const lsamgdd_csr* a, void** out_matrix, char* err, size_t errlen) {
+  if (out_matrix) *out_matrix = nullptr;
+  return guarded(err, errlen, [&] {
+    check_csr(a, "matrix_create");
+    if (!out_matrix) raise(LSAMGDD_ERR_INPUT, "matrix_create: null output");
+    require_device();
+    auto h = std::make_unique<MatrixHandle>();
+    LSB_CUDA(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+    if (a->memory == LSAMGDD_DEVICE) wait_for_caller(h->s);
+    csr_upload(h->m, a, h->s);
+    LSB_CUDA(cudaStreamSynchronize(h->s));
+    *out_matrix = h.release();
+  });
+}
+
+int lsamgdd_matrix_spmv(void* matrix, int32_t transpose, const double* x, double* y, int32_t memory, char* err,
+                        size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!matrix) raise(LSAMGDD_ERR_INPUT, "null matrix handle");
+    require_device();
+    MatrixHandle& h = *static_cast<MatrixHandle*>(matrix);
+    std::lock_guard<std::mutex> lock(h.mu);  // one stream per handle
+    if (!transpose && !h.has_sell) {
+      sell_from_csr(h.m, h.sell, h.s);
+      h.has_sell = true;
+    }
+    if (transpose && !h.has_sell_t) {
+      DevCsr t;
+      csr_transpose(h.m, t, h.s);
+      sell_from_csr(t, h.sell_t, h.s);
+      h.has_sell_t = true;
+    }
+    const Sell& sp = transpose ? h.sell_t : h.sell;
+    with_vectors(h.s, x, sp.nc, y, sp.nr, memory, [&](const double* dx, double* dy) { sell_spmv(sp, dx, dy, nullptr, h.s); });
+  });
 }
 
 int lsamgdd_matrix_export(const void* matrix, int64_t sizes[3], int64_t* offsets, int64_t* cols, double* vals) {

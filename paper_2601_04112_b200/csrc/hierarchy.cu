@@ -412,9 +412,10 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
   }
   stage("upload_galerkin_A0", t0);
   const uint64_t probe = p->probe_levels;
-  while (h->levels.size() < p->max_levels && static_cast<uint64_t>(h->levels.back().A.nr) > p->coarse_size &&
+  const int64_t lvl0 = static_cast<int64_t>(p->level_offset);  // global index of this hierarchy's first level
+  while (h->levels.size() + lvl0 < p->max_levels && static_cast<uint64_t>(h->levels.back().A.nr) > p->coarse_size &&
          (probe == 0 || h->levels.size() <= probe)) {
-    const int64_t ell = static_cast<int64_t>(h->levels.size()) - 1;
+    const int64_t ell = static_cast<int64_t>(h->levels.size()) - 1 + lvl0;
     Level& cur = h->levels.back();
     t0 = Clock::now();
     HostCsr a_host = download(cur.A, s);

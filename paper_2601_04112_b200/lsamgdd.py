@@ -123,6 +123,7 @@ class LevelParams:
     level0_max_modes: int = 0
     device: int = 0
     probe_levels: int = 0  # > 0: build that many fine levels and stop (stage-wise parity / timing at full size)
+    level_offset: int = 0  # > 0: the factor is that level of a hierarchy whose finer levels were built elsewhere
 
     def to_abi(self) -> tuple[abi.Params, Optional[np.ndarray]]:
         keep = None
@@ -132,7 +133,7 @@ class LevelParams:
             pre_sweeps=self.pre_sweeps, post_sweeps=self.post_sweeps, gevp_variant=self.gevp_variant,
             keep_spectra=1 if self.keep_spectra else 0, level0_overlap=self.level0_overlap,
             thresh_override=float(self.thresh_override), level0_max_modes=self.level0_max_modes, device=self.device,
-            probe_levels=int(self.probe_levels),
+            probe_levels=int(self.probe_levels), level_offset=int(self.level_offset),
         )
         if self.level0_partition is not None:
             keep = np.ascontiguousarray(self.level0_partition, dtype=np.int64)
