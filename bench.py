@@ -19,8 +19,11 @@ rtol 1e-8 with the V(1,1) cycle. Metric: unknowns/s = n / (T_setup + T_solve).
   ratio.
 
 Multi-GPU: ``python -m torch.distributed.run --nproc-per-node N bench.py
---gpus N`` runs N independent replicas (round 1 is
-"replicas only"); value = N·n / max-over-ranks step time.
+--gpus N`` runs the row/aggregate partition of paper_2601_04112_b200/dist.py
+(DESIGN.md §6): the same 1024² problem split into N strips, one process per
+GPU, halo exchange / reverse-halo add / dot all-reduce / gathered coarse
+vector over NCCL; value = n / max-over-ranks step time (``"scaling":
+"strong"``). The N = 1 line is the single-GPU library path.
 """
 from __future__ import annotations
 
@@ -121,8 +124,10 @@ def dist_setup(n_gpus: int):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         import torch
 
-        # NCCL between the GPUs of the box; gloo only for the CPU tests of this plumbing
-        dist.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        # NCCL between the GPUs of the box; gloo for the CPU tests of this plumbing and for the
+        # one-GPU plumbing check of the partitioned path (LSB_DIST_BACKEND=gloo: the ranks share a GPU)
+        backend = os.environ.get("LSB_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        dist.init_process_group(backend)
         pg = dist
     return world, rank, local, pg
 
@@ -227,6 +232,83 @@ def cpu_baseline_sample(cfg, iters: int) -> dict:
             "stages_ms": r["stages_ms"]}
 
 
+def run_partitioned(args, cfg, world, rank, local, pg, dev) -> None:
+    """N > 1: the strip partition (strong scaling). One step = partitioned setup (level-0 stages
+    per strip, all-gathered P0, replicated coarse hierarchy) + distributed PCG to 1e-8."""
+    import torch
+
+    from paper_2601_04112_b200 import dist as pdist, lsamgdd
+
+    comm = pdist.TorchComm(pg, dev if pg.get_backend() == "nccl" else "cpu")
+    over = {"device": local}
+    if "thresh_override" not in dict(cfg.params) or not dict(cfg.params).get("thresh_override"):
+        # the reference's threshold rule needs the global colour count and multiplicity bound
+        # (splitting.hpp:170-180): take them from a level-0 probe of the whole problem on rank 0
+        thr = torch.zeros(1, dtype=torch.float64, device=dev)
+        if rank == 0:
+            hp = lsamgdd.setup(cfg, lsamgdd.params_for(cfg, probe_levels=1, device=local))
+            thr[0] = hp.summary[0].thresh
+            del hp
+        if pg.get_backend() != "nccl":
+            thr = thr.cpu()
+        pg.broadcast(thr, 0)
+        over["level0_thresh"] = float(thr.item())
+    lvl0_thr = over.pop("level0_thresh", None)
+
+    def step():
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        solver = pdist.build_gpu_solver(cfg, comm, over, level0_thresh=lvl0_thr)
+        t1 = time.perf_counter()
+        x, its, conv, hist = solver.pcg(cfg.rhs[solver.plan.own], 1e-8, 1000)
+        torch.cuda.synchronize()
+        t2 = time.perf_counter()
+        levels = solver.ops.h_coarse.num_levels + 1
+        solver.ops.close()
+        return (t2 - t0) * 1e3, (t1 - t0) * 1e3, (t2 - t1) * 1e3, its, conv, levels
+
+    for _ in range(args.warmup):
+        step()
+    c0 = lib_launches()
+    with ClockSampler(local) as clk:
+        recs = []
+        for _ in range(args.steps):
+            pg.barrier()
+            recs.append(step())
+    launches = (lib_launches() - c0) // max(args.steps, 1)
+    rdev = dev if pg.get_backend() == "nccl" else torch.device("cpu")
+    ms_step = barrier_max(pg, statistics.mean(r[0] for r in recs), rdev)
+    setup_ms = barrier_max(pg, statistics.mean(r[1] for r in recs), rdev)
+    solve_ms = barrier_max(pg, statistics.mean(r[2] for r in recs), rdev)
+    value = cfg.n / (ms_step / 1e3)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "grid": cfg.meta["grid"], "n": cfg.n, "m": cfg.m, "nnz_G": cfg.nnz,
+                   "levels": recs[-1][5], "pcg_iterations": recs[-1][3], "converged": bool(recs[-1][4]),
+                   "setup_ms": setup_ms, "solve_ms": solve_ms,
+                   "l2": "inputs larger than L2 (G0 CSR %.0f MB > 126 MB)" % ((cfg.g_rowptr.nbytes + cfg.g_cols.nbytes + cfg.g_vals.nbytes) / 1e6),
+                   "parallelism": f"{world} strips of level-0 aggregates (halo exchange, reverse-halo add, dot all-reduce, "
+                                  "gathered coarse vector; coarse hierarchy replicated; vectors staged through the host)"},
+        "roofline": None,
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": int(cfg.g_rowptr.nbytes + cfg.g_cols.nbytes + cfg.g_vals.nbytes + cfg.rhs.nbytes),
+                "d2h_bytes_per_step": int(8 * cfg.n), "ms_per_step": ms_step,
+                "note": "the partitioned path takes host buffers: every operator call copies its strip vectors in and out"},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    pg.destroy_process_group()
+
+
+def lib_launches() -> int:
+    from paper_2601_04112_b200 import lsamgdd
+
+    return int(lsamgdd.library().lsamgdd_launch_count())
+
+
 def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -250,10 +332,14 @@ def main() -> None:
 
     from paper_2601_04112_b200 import abi, configs, lsamgdd
 
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = lsamgdd.library()
     cfg = configs.config(args.config, args.grid)
+    if world > 1:
+        run_partitioned(args, cfg, world, rank, local, pg, dev)
+        return
     params = lsamgdd.params_for(cfg, device=local)
     pabi, keep = params.to_abi()
     n, m, nnz = cfg.n, cfg.m, cfg.nnz

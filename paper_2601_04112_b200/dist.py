@@ -450,14 +450,19 @@ def gather_p0(plan: StripPlan, p_loc: sp.csr_matrix, n: int, comm: Comm):
 
 
 def build_gpu_solver(cfg, comm: Comm, params_over: Optional[dict] = None,
-                     spgemm: Optional[Callable] = None) -> DistSolver:
-    """The partitioned solver of a BASELINE config on this rank's GPU (collective)."""
-    from . import lsamgdd
+                     spgemm: Optional[Callable] = None, level0_thresh: Optional[float] = None) -> DistSolver:
+    """The partitioned solver of a BASELINE config on this rank's GPU (collective).
 
+    level0_thresh: the global level-0 threshold when the config leaves it to the reference's
+    rule (eigen_threshold needs the global colour count and multiplicity bound, splitting.hpp:
+    170-180); the strips then use it directly, the coarse hierarchy keeps the rule."""
     g = sp.csr_matrix((cfg.g_vals, cfg.g_cols, cfg.g_rowptr), shape=(cfg.m, cfg.n))
     overlap = int(dict(cfg.params).get("level0_overlap", 1))
     plan = build_plan(g, cfg.level0_partition, int(cfg.level0_n_aggregates), overlap, comm)
-    ops = GpuOps(plan, cfg, comm, params_over)
+    strip_over = dict(params_over or {})
+    if level0_thresh is not None:
+        strip_over["thresh_override"] = float(level0_thresh)
+    ops = GpuOps(plan, cfg, comm, strip_over)
     p0, coff = gather_p0(plan, ops.p_loc, cfg.n, comm)
     g1 = (spgemm or gpu_spgemm)(g, p0)
     ops.set_coarse(g1, cfg, params_over)
