@@ -602,6 +602,27 @@ int ref_eigen_threshold(double kappa, int64_t kc, int64_t n_mult, double* out, c
   return guarded(err, errlen, [&] { *out = eigen_threshold(kappa, kc, n_mult); });
 }
 
+// mmio.hpp round trips for the tests of paper_2601_04112_b200/mmio.py
+int ref_mm_write(const lsamgdd_csr* m, const char* path, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] { mm_write(path, from_csr(m)); });
+}
+
+int ref_mm_read(const char* path, int64_t sizes[3], int64_t* off, int64_t* col, double* val, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] { export_csr(mm_read(path), sizes, off, col, val); });
+}
+
+int ref_mm_write_vector(const double* v, int64_t n, const char* path, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] { mm_write_vector(path, Vector(v, v + n)); });
+}
+
+int ref_mm_read_vector(const char* path, int64_t* n, double* out, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    const Vector v = mm_read_vector(path);
+    *n = static_cast<int64_t>(v.size());
+    if (out) std::memcpy(out, v.data(), v.size() * sizeof(double));
+  });
+}
+
 void ref_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out) {
   std::mt19937_64 gen(seed);
   std::uniform_real_distribution<double> dist(lo, hi);

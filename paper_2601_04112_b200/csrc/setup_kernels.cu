@@ -19,6 +19,14 @@
 #include "dense_dev.cuh"
 #include "setup_kernels.cuh"
 
+// Diagnostics (per-phase cycle counters, the tiled-Gram cross-check) exist only in builds made
+// with `make DIAG=1` (-DLSB_DIAG); the product library reads no environment variable.
+#ifdef LSB_DIAG
+#define LSB_DIAG_ENV(name) (getenv(name) != nullptr)
+#else
+#define LSB_DIAG_ENV(name) false
+#endif
+
 namespace lsb {
 
 namespace {
@@ -379,12 +387,26 @@ __global__ void __launch_bounds__(WPB * 32) k_gevp_warp(GevpArgs g) {
   for (int idx = blockIdx.x * WPB + warp; idx < g.n_list; idx += gridDim.x * WPB) gevp_problem(t, g, idx, ws);
 }
 
+// Mid-size subdomains (workspace beyond the shared-memory warp class, eigenproblems up to
+// kWarpGlobMax): one warp per problem with its workspace in global memory (L1/L2-resident), many
+// problems per SM — the per-problem latency of the warp team matches the one-CTA-per-problem
+// kernels at these sizes (measured), the occupancy is 16 problems per SM instead of one.
+template <int WPB>
+__global__ void __launch_bounds__(WPB * 32) k_gevp_warp_g(GevpArgs g) {
+  WarpTeam t;
+  const int warp = threadIdx.x >> 5;
+  const int slot = blockIdx.x * WPB + warp;
+  double* ws = g.gws + int64_t(slot) * g.ws_stride;
+  for (int idx = slot; idx < g.n_list; idx += gridDim.x * WPB) gevp_problem(t, g, idx, ws);
+}
+
 // shared doubles for the pipelined Jacobi: 207 KiB dynamic + the kernels'
 // static shared arrays (15 KiB) stay within the 227 KiB per CTA
 constexpr int64_t kFastCap = 26500;
 constexpr int kWaveCluster = 4;  // CTAs per cluster of the wavefront Jacobi: 1 leader + 3 replay CTAs
-constexpr int64_t kWaveClassMin = 128;  // subdomains with max(nω, nΓ) >= this run in clusters
+constexpr int64_t kWaveClassMin = 100;  // subdomains with max(nω, nΓ) >= this run in clusters
 constexpr int64_t kWaveSmallMax = 256;  // ... of 2 CTAs up to this size, of 4 CTAs above
+constexpr int64_t kWarpGlobMax = 99;    // below the cluster class: warp teams with global workspaces
 constexpr int kWaveMinN = 1;            // ... where every eigensolve takes the wavefront path
 
 template <bool SMEM>
@@ -1039,7 +1061,7 @@ int dense_sym_eig(int64_t n, const double* h_a, double* h_vals, double* h_vecs, 
     ctl.zero(s);
     DBuf<long long> prof(16, s);
     prof.zero(s);
-    const bool want_prof = getenv("LSB_WAVE_PROF") != nullptr;  // diagnostic: phase cycle counters of this test hook
+    const bool want_prof = LSB_DIAG_ENV("LSB_WAVE_PROF");  // diagnostic: phase cycle counters of this test hook
     if (want_prof) {
       long long* pp = prof.get();
       LSB_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(ctl.get()) + offsetof(WaveCtl, prof), &pp, sizeof(pp),
@@ -1228,12 +1250,12 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
   status.zero(s);
   nspec.zero(s);
   {
-    const int chk = getenv("LSB_GRAM_CHECK") ? 1 : 0;
+    const int chk = LSB_DIAG_ENV("LSB_GRAM_CHECK") ? 1 : 0;
     unsigned long long z[8] = {0};
     LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_check, &chk, sizeof(chk), 0, cudaMemcpyHostToDevice, s));
     LSB_CUDA(cudaMemcpyToSymbolAsync(g_gram_bad, z, sizeof(z), 0, cudaMemcpyHostToDevice, s));
   }
-  const bool prof_on = getenv("LSB_GEVP_PROF") != nullptr;
+  const bool prof_on = LSB_DIAG_ENV("LSB_GEVP_PROF");
   DBuf<long long> eprof(prof_on ? 8 : 1, s);
   if (prof_on) {
     eprof.zero(s);
@@ -1304,14 +1326,22 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
       const int64_t nw = hoo[a + 1] - hoo[a], ng = hgo[a + 1] - hgo[a], mx = std::max(nw, ng);
       return mx >= kWaveClassMin && mx <= kWaveMaxN;
     };
-    std::vector<int32_t> aggs, big;
-    for (int64_t a = a0; a < a1; ++a) (wave_class(a) ? big : aggs).push_back(static_cast<int32_t>(a));
+    // mid-size subdomains: warp teams with global workspaces
+    auto mid_class = [&](int64_t a) {
+      const int64_t nw = hoo[a + 1] - hoo[a], ng = hgo[a + 1] - hgo[a], mx = std::max(nw, ng);
+      return ws_class(need[a]) >= 1 && mx <= kWarpGlobMax && !wave_class(a);
+    };
+    std::vector<int32_t> aggs, big, mid;
+    for (int64_t a = a0; a < a1; ++a)
+      (wave_class(a) ? big : mid_class(a) ? mid : aggs).push_back(static_cast<int32_t>(a));
     // classes decide the list order; panel scratch offsets follow that order
     std::vector<int32_t> order;
     {
       std::vector<int32_t> cls[3];
       for (int32_t a : aggs) cls[ws_class(need[a])].push_back(a);
       for (int c = 0; c < 3; ++c) order.insert(order.end(), cls[c].begin(), cls[c].end());
+      std::stable_sort(mid.begin(), mid.end(), [&](int32_t x, int32_t y) { return need[x] > need[y]; });
+      order.insert(order.end(), mid.begin(), mid.end());
       // largest first: the longest problems start first (the > 256 class launches before the <= 256 class)
       std::stable_sort(big.begin(), big.end(), [&](int32_t x, int32_t y) { return need[x] > need[y]; });
       auto big_mx = [&](int32_t a) { return std::max(hoo[a + 1] - hoo[a], hgo[a + 1] - hgo[a]); };
@@ -1351,6 +1381,30 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     g.pre_off = pre.get() ? pre_off.get() : nullptr;
     std::vector<int32_t> lo;
     if (!aggs.empty()) launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, s);
+    DBuf<int32_t> mid_list;
+    DBuf<double> mid_ws;
+    if (!mid.empty()) {
+      constexpr int WPB = 4;
+      const int base = static_cast<int>(lo.size());
+      const int cnt = static_cast<int>(mid.size());
+      int64_t wmax = 0;
+      for (int32_t a : mid) wmax = std::max(wmax, need[a]);
+      wmax = r2(wmax);
+      // 16 warps (problems) per SM; bound the footprint to ~2 GiB
+      const int64_t slots = std::max<int64_t>(WPB, std::min<int64_t>({int64_t(ceil_div(cnt, WPB)) * WPB, int64_t(sm_count()) * 16,
+                                                                      ((int64_t(1) << 28) / std::max<int64_t>(wmax, 1)) / WPB * WPB}));
+      mid_list.upload(mid, s);
+      mid_ws.alloc(slots * wmax, s);
+      GevpArgs gm2 = g;
+      gm2.list = mid_list.get();
+      gm2.list_base = base;
+      gm2.n_list = cnt;
+      gm2.ws_stride = wmax;
+      gm2.gws = mid_ws.get();
+      k_gevp_warp_g<WPB><<<static_cast<int>(slots / WPB), WPB * 32, 0, s>>>(gm2);
+      LSB_LAUNCH();
+      lo.insert(lo.end(), mid.begin(), mid.end());
+    }
     // cluster classes: subdomains up to 256 run on 2-CTA clusters (16 replay warps cover
     // their 2·NB row groups), larger ones on 4-CTA clusters
     std::vector<DBuf<int32_t>> big_lists;
@@ -1427,7 +1481,7 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     fprintf(stderr, "   large-n Jacobi steps %lld, rotations %lld\n", he[6], he[7]);
     LSB_CUDA(cudaMemcpyToSymbol(g_eig_prof, &np, sizeof(np)));
   }
-  if (getenv("LSB_GRAM_CHECK") && pre.get()) {
+  if (LSB_DIAG_ENV("LSB_GRAM_CHECK") && pre.get()) {
     unsigned long long hb[8];
     LSB_CUDA(cudaMemcpyFromSymbolAsync(hb, g_gram_bad, sizeof(hb), 0, cudaMemcpyDeviceToHost, s));
     LSB_CUDA(cudaStreamSynchronize(s));

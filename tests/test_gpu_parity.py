@@ -483,3 +483,26 @@ def test_partitioned_solve_on_gpu_matches_single_gpu(gpu, name, grid, over, worl
         assert nl == h.num_levels - 1  # the replicated coarse hierarchy holds the levels >= 1
     assert np.linalg.norm(e - e_ref) <= 1e-10 * np.linalg.norm(e_ref)
     assert np.linalg.norm(x - x_ref) <= 1e-8 * np.linalg.norm(x_ref)
+
+
+def test_cli_report_schema_from_a_gpu_run(gpu, tmp_path):
+    """The reference CLI's outcome document (lsamgdd_cli.cpp:182-200) and spectra dump from a B200 run."""
+    import time
+
+    from paper_2601_04112_b200 import report
+    cfg = configs.config("c1")
+    t0 = time.perf_counter()
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg, keep_spectra=True))
+    setup_s = time.perf_counter() - t0
+    x, rep = lsamgdd.pcg(h, cfg.rhs, 1e-8, 1000)
+    doc = report.outcome_json("c1", h, rep, setup_s)
+    assert list(doc) == ["label", "converged", "iterations", "rho", "iters_to_tenth", "op_complexity", "levels", "setup_s",
+                         "solve_s", "residual_history", "hierarchy"]
+    assert doc["converged"] and doc["iterations"] == 18 and doc["levels"] == 2
+    assert list(doc["hierarchy"][0]) == ["level", "dim", "nnz", "aggregates", "colors", "multiplicity", "thresh", "modes_kept"]
+    assert doc["hierarchy"][0]["aggregates"] == 256 and len(doc["residual_history"]) == 19
+    assert report.csv_row(0.5, doc).count(",") == 7
+    path = tmp_path / "spectra.csv"
+    report.write_spectra_csv(h, str(path))
+    lines = path.read_text().splitlines()
+    assert lines[0] == "level,aggregate,index,eigenvalue" and len(lines) == 1 + 256 * 16
