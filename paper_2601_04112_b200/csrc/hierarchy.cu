@@ -755,7 +755,11 @@ PcgResult pcg(const Hierarchy& h, SolveWs& ws, const Sell& g, const Sell& gt, co
     *stats = lsamgdd_kernel_stats{};
     stats->schwarz_ms = sw_ms;
     stats->schwarz_bytes = static_cast<double>(graph_launches) * (h.levels.size() > 1 ? h.levels[0].sm.bytes_ras + h.levels[0].sm.bytes_rast : 0.0);
-    stats->schwarz_launches = graph_launches * (h.levels.size() > 1 ? static_cast<int64_t>(h.levels[0].sm.color_off.size()) : 0);
+    // launches per RAS + RAS-T pair: 3 on the TMA path (RAS, RAS-T, slot gather), else 1 + the colour launches
+    const int64_t per_pair = h.levels.size() > 1
+                                 ? (h.levels[0].sm.n_slots > 0 ? 3 : static_cast<int64_t>(h.levels[0].sm.color_off.size()))
+                                 : 0;
+    stats->schwarz_launches = graph_launches * per_pair;
     // PCG operator y = Gᵀ(G p) (SpMV with G, then with the stored Gᵀ fused with ⟨p, y⟩):
     // algorithmic bytes B(spmv_G) + B(spmvT_G) of SURVEY.md §8(d)
     const double nnz = static_cast<double>(g.nnz), mm = static_cast<double>(g.nr), nn = static_cast<double>(n);
