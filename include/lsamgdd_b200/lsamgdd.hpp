@@ -400,6 +400,35 @@ inline Vector apply(const Smoother& s, const Vector& r, SchwarzMode mode) {
 
 // pcg with caller functors (krylov.hpp:42): the reference's host loop, unchanged
 using lsamgdd::pcg;
+// precond_spectrum (krylov.hpp:101-143): a dense host probe capped at 2000 unknowns, unchanged;
+// the functors it is given may be built from the device operators above
+using lsamgdd::precond_spectrum;
+
+// TwoLevelAdditive (hierarchy.hpp:234-254), a spectrum-study operator, not part of the solve:
+// the coarse correction runs through the device SpMVs on the level-0 P mirror; the ASM sweep —
+// which needs the full Ω×Ω inverses the device smoother does not keep (it stores the ω columns
+// RAS and RAS-T read) — runs through the reference's host smoother built from the level-0 mirrors.
+class TwoLevelAdditive {
+ public:
+  explicit TwoLevelAdditive(const Hierarchy& h) : h_(h) {
+    if (h.levels.size() < 2) throw InputError("TwoLevelAdditive: hierarchy has fewer than two levels");
+    coarse_ = factor_spd_block(to_dense(h.levels[1].A), "first coarse-level matrix");
+    smoother_ = lsamgdd::build_smoother(h.levels[0].A, h.levels[0].topology, SchwarzMode::ASM);
+  }
+  Vector apply_to(const Vector& r) const {
+    const Level& fine = h_.levels[0];
+    Vector coarse = b200::spmv_transpose(fine.P, r);
+    coarse_.solve_inplace(coarse);
+    Vector y = b200::spmv(fine.P, coarse);
+    axpy(1.0, lsamgdd::apply(smoother_, r, SchwarzMode::ASM), y);
+    return y;
+  }
+
+ private:
+  const Hierarchy& h_;
+  CholeskyFactor coarse_;
+  SchwarzSmoother smoother_;
+};
 
 inline double operator_complexity(const Hierarchy& h) {
   double v = 0.0;

@@ -154,6 +154,32 @@ void check_vcycle_spd() {  // acceptance.cpp:208-260 (symmetry and positivity of
          "the V-cycle is symmetric and positive on random probes, worst asymmetry " + std::to_string(worst) + " " + failure);
 }
 
+void check_two_level_spectrum() {  // acceptance.cpp:264-295
+  bool pass = false;
+  std::string detail;
+  try {
+    const auto sys = make_aniso(16, 1.0, 0.0);
+    LevelParams params;
+    params.coarse_size = 100;
+    const hot::Hierarchy h = hot::setup(sys.G, params);
+    const hot::TwoLevelAdditive two(h);
+    const double tau = h.levels[0].thresh;
+    const double k_c = static_cast<double>(h.levels[0].topology.n_colors);
+    const double lower = 1.0 / (2.0 + (2.0 * k_c + 1.0) * tau);
+    const double upper = k_c + 1.0;
+    const auto apply_a = [&sys](const Vector& v) { return hot::spmv(sys.A, v); };
+    const auto apply_b = [&two](const Vector& r) { return two.apply_to(r); };
+    const auto [lo, hi] = hot::precond_spectrum(apply_a, apply_b, sys.A.n_rows());
+    const double slack = 1e-10;
+    pass = lo >= lower - slack && hi <= upper + slack;
+    detail = "measured [" + std::to_string(lo) + ", " + std::to_string(hi) + "] within [" + std::to_string(lower) + ", " +
+             std::to_string(upper) + "], k_c=" + std::to_string(k_c) + ", tau=" + std::to_string(tau);
+  } catch (const lsamgdd::Error& e) {
+    detail = e.what();
+  }
+  record(5, pass, "additive two-level spectrum on the 16x16 isotropic grid: " + detail);
+}
+
 void check_direct_oracle() {  // acceptance.cpp:451-495 (the rotated-anisotropy systems)
   bool pass = true;
   double worst = 0.0;
@@ -197,6 +223,7 @@ int main() {
   check_factor_propagation();
   check_ras_adjointness();
   check_vcycle_spd();
+  check_two_level_spectrum();
   check_direct_oracle();
   // spectra_csv (hierarchy.hpp:121-127): same header and row format as the reference's dump
   {
