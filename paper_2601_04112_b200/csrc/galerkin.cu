@@ -203,8 +203,6 @@ __global__ void k_tiles(const uint64_t* key, const int32_t* head, const int32_t*
   }
 }
 
-constexpr int kTileRows = 32;     // rows of G staged per step
-constexpr int kTileThreads = 256;
 constexpr int kSub = 32;          // output sub-tile edge
 
 struct TileArgs {
@@ -225,22 +223,26 @@ struct TileArgs {
   int64_t n_items;
 };
 
-
-// One CTA per (tile, sub-tile): stages kTileRows shared rows of the a- and
+// One CTA per (tile, sub-tile): stages ROWS shared rows of the a- and
 // b-segments (dense, with a presence flag = stored entry), then every thread
-// advances its outputs over those rows in ascending order.
-__global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
+// advances its outputs over those rows in ascending order. Two shapes: 256
+// threads × 32 rows where the items fill the SMs several times over, 512
+// threads × 64 rows (two outputs per thread, four rows in flight per warp) on
+// the coarse levels, where a handful of items walk millions of rows each.
+template <int THREADS, int ROWS>
+__global__ void __launch_bounds__(THREADS) k_gtg_tile(TileArgs g) {
   // Segments are staged dense (absent entries = +0: adding the ±0 products
   // leaves every sum unchanged, it starts at +0 and never becomes -0) with a
   // presence mask per row; an output exists in the Symbolic pattern iff some
   // row holds both of its entries.
   static_assert(kSub == 32, "presence masks are 32-bit");
-  __shared__ double sa[kTileRows][kSub];
-  __shared__ double sb[kTileRows][kSub];
-  __shared__ unsigned ma[kTileRows], mb[kTileRows];
-  constexpr int kPer = kSub * kSub / kTileThreads;
-  constexpr int kIStep = kTileThreads / kSub;  // output rows of a thread: i0 + kIStep*q, column j
-  const int lane = threadIdx.x & 31;
+  __shared__ double sa[ROWS][kSub];
+  __shared__ double sb[ROWS][kSub];
+  __shared__ unsigned ma[ROWS], mb[ROWS];
+  constexpr int kPer = kSub * kSub / THREADS;
+  constexpr int kIStep = THREADS / kSub;  // output rows of a thread: i0 + kIStep*q, column j
+  constexpr int kWarps = THREADS / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int ti = threadIdx.x / kSub, tj = threadIdx.x % kSub;
   for (int64_t w = blockIdx.x; w < g.n_items; w += gridDim.x) {
     const int t = g.wi_tile[w];
@@ -254,59 +256,56 @@ __global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
     unsigned touched = 0u;
 #pragma unroll
     for (int q = 0; q < kPer; ++q) acc[q] = 0.0;
-    for (int64_t rb = r0; rb < r1; rb += kTileRows) {
-      const int nr = static_cast<int>(r1 - rb < kTileRows ? r1 - rb : kTileRows);
-      for (int q = threadIdx.x; q < nr * kSub; q += blockDim.x) {  // outputs beyond bi/bj are discarded
-        const int rr = q / kSub, c = q % kSub;
-        if (c < bi) sa[rr][c] = 0.0;
-        if (c < bj) sb[rr][c] = 0.0;
+    for (int64_t rb = r0; rb < r1; rb += ROWS) {
+      const int nr = static_cast<int>(r1 - rb < ROWS ? r1 - rb : ROWS);
+      // a warp owns its rows: clear, scatter the segment entries, publish the masks
+      int64_t lo[(ROWS + kWarps - 1) / kWarps], hi[(ROWS + kWarps - 1) / kWarps];
+#pragma unroll
+      for (int u = 0; u < (ROWS + kWarps - 1) / kWarps; ++u) {
+        const int rr = warp + u * kWarps;
+        lo[u] = hi[u] = 0;
+        if (rr < nr) {
+          const int64_t r = __ldg(g.rows + rb + rr);
+          lo[u] = __ldg(g.goff + r);
+          hi[u] = __ldg(g.goff + r + 1);
+          sa[rr][lane] = 0.0;
+          sb[rr][lane] = 0.0;
+        }
       }
-      if (threadIdx.x < kTileRows) {
-        ma[threadIdx.x] = 0u;
-        mb[threadIdx.x] = 0u;
-      }
-      __syncthreads();
-      for (int rr = threadIdx.x >> 5; rr < nr; rr += blockDim.x >> 5) {
-        // one coalesced pass over the row
-        const int64_t r = g.rows[rb + rr];
-        const int64_t lo = g.goff[r], hi = g.goff[r + 1];
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < (ROWS + kWarps - 1) / kWarps; ++u) {
+        const int rr = warp + u * kWarps;
+        if (rr >= nr) continue;
         unsigned bits_a = 0u, bits_b = 0u;
-        for (int64_t k = lo + lane; k < hi; k += 32) {
-          const int col = g.gcol[k];
+#pragma unroll 2
+        for (int64_t k = lo[u] + lane; k < hi[u]; k += 32) {  // one coalesced pass over the row
+          const int col = __ldg(g.gcol + k);
+          const double v = __ldg(g.gval + k);
           const unsigned ea = static_cast<unsigned>(col - ca), eb = static_cast<unsigned>(col - cb);
-          if (ea < static_cast<unsigned>(bi) || eb < static_cast<unsigned>(bj)) {
-            const double v = g.gval[k];
-            if (ea < static_cast<unsigned>(bi)) {
-              sa[rr][ea] = v;
-              bits_a |= 1u << ea;
-            }
-            if (eb < static_cast<unsigned>(bj)) {
-              sb[rr][eb] = v;
-              bits_b |= 1u << eb;
-            }
+          if (ea < static_cast<unsigned>(bi)) {
+            sa[rr][ea] = v;
+            bits_a |= 1u << ea;
+          }
+          if (eb < static_cast<unsigned>(bj)) {
+            sb[rr][eb] = v;
+            bits_b |= 1u << eb;
           }
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          bits_a |= __shfl_xor_sync(0xffffffffu, bits_a, o);
-          bits_b |= __shfl_xor_sync(0xffffffffu, bits_b, o);
-        }
+        bits_a = __reduce_or_sync(0xffffffffu, bits_a);
+        bits_b = __reduce_or_sync(0xffffffffu, bits_b);
         if (lane == 0) {
           ma[rr] = bits_a;
           mb[rr] = bits_b;
         }
       }
       __syncthreads();
+#pragma unroll 4
       for (int rr = 0; rr < nr; ++rr) {
-        const unsigned am = ma[rr];
         const double yb = sb[rr][tj];
-        const bool hb = ((mb[rr] >> tj) & 1u) != 0u;
+        touched |= ((mb[rr] >> tj) & 1u) ? ma[rr] : 0u;  // a-entries met by a stored b-entry of column tj
 #pragma unroll
-        for (int q = 0; q < kPer; ++q) {
-          const int i = ti + kIStep * q;
-          acc[q] += sa[rr][i] * yb;
-          if (hb && ((am >> i) & 1u)) touched |= 1u << q;
-        }
+        for (int q = 0; q < kPer; ++q) acc[q] += sa[rr][ti + kIStep * q] * yb;
       }
       __syncthreads();
     }
@@ -318,9 +317,8 @@ __global__ void __launch_bounds__(kTileThreads) k_gtg_tile(TileArgs g) {
       if (i >= bi || j >= bj) continue;
       const int64_t e = int64_t(i0 + i) * kb + (j0 + j);
       tv[e] = acc[q];
-      tm[e] = ((touched >> q) & 1u) ? 1 : 0;
+      tm[e] = ((touched >> i) & 1u) ? 1 : 0;
     }
-    __syncthreads();
   }
 }
 
@@ -495,8 +493,11 @@ void galerkin_gtg(const DevCsr& gn, const DevRowSets& rs, int64_t n_agg, const D
                 rows.get(), d_tval_off.get(), tval.get(), tmask.get(), d_wt.get(), d_wi.get(), d_wj.get(),
                 static_cast<int64_t>(wt.size())};
   if (!wt.empty()) {
-    k_gtg_tile<<<static_cast<int>(std::min<int64_t>(static_cast<int64_t>(wt.size()), sm_count() * 8)), kTileThreads, 0,
-                 s>>>(targ);
+    const int64_t items = static_cast<int64_t>(wt.size());
+    if (items <= 2 * int64_t(sm_count()))
+      k_gtg_tile<512, 64><<<static_cast<int>(std::min<int64_t>(items, sm_count())), 512, 0, s>>>(targ);
+    else
+      k_gtg_tile<256, 32><<<static_cast<int>(std::min<int64_t>(items, sm_count() * 8)), 256, 0, s>>>(targ);
     LSB_LAUNCH();
   }
   // 4) per aggregate tile lists sorted by partner, then rows of A

@@ -13,6 +13,7 @@
 #include <iostream>
 #include <memory>
 #include <numeric>
+#include <thread>
 
 #include "galerkin.cuh"
 #include "hierarchy.cuh"
@@ -363,6 +364,10 @@ Hierarchy::~Hierarchy() {
     cudaStreamSynchronize(stream);
     cudaStreamDestroy(stream);
   }
+  if (side_stream) {
+    cudaStreamSynchronize(side_stream);
+    cudaStreamDestroy(side_stream);
+  }
 }
 
 Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
@@ -395,6 +400,8 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
   } pool_keep(p->device);
   LSB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   cudaStream_t s = h->stream;
+  LSB_CUDA(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));
+  cudaStream_t s2 = h->side_stream;
   auto stage = [&](const char* name, Clock::time_point t0) {
     LSB_CUDA(cudaStreamSynchronize(s));
     h->timings.push_back({name, ms_since(t0)});
@@ -430,11 +437,28 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
     build_topology(a_host, asg, n_agg, (ell == 0 && p->level0_overlap >= 2) ? 2 : 1, cur);
     upload_topology(cur, asg, s);
     stage("aggregation_topology", t0);
+    // The Schwarz blocks depend on A_l and the topology only: they are factorised on a second
+    // stream by a side thread while this one runs the local eigenproblems (which leave most SMs
+    // idle on the coarse levels). Joined before the Galerkin products.
     t0 = Clock::now();
-    build_smoother(cur.A, cur.topo, cur.h_omega_off, cur.h_gamma_off, cur.colors, cur.n_colors, cur.sm, s, &cur.h_gamma);
-    sell_from_csr(cur.A, cur.A_sell, s);
-    stage("build_smoother", t0);
-    t0 = Clock::now();
+    std::exception_ptr sm_err;
+    std::thread sm_thread([&, dev = p->device] {
+      try {
+        LSB_CUDA(cudaSetDevice(dev));
+        build_smoother(cur.A, cur.topo, cur.h_omega_off, cur.h_gamma_off, cur.colors, cur.n_colors, cur.sm, s2,
+                       &cur.h_gamma);
+        sell_from_csr(cur.A, cur.A_sell, s2);
+        LSB_CUDA(cudaStreamSynchronize(s2));
+      } catch (...) {
+        sm_err = std::current_exception();
+      }
+    });
+    struct Joiner {
+      std::thread& t;
+      ~Joiner() {
+        if (t.joinable()) t.join();
+      }
+    } joiner{sm_thread};
     DevRowSets rs;
     row_sets(cur.G, cur.topo, rs, s);
     if (rs.empty_rows > 0)
@@ -458,6 +482,10 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
         cur.ip.coarse_off.get(), n_agg, cur.col_agg.get());
     LSB_LAUNCH();
     stage("local_gevp", t0);
+    t0 = Clock::now();
+    sm_thread.join();
+    if (sm_err) std::rethrow_exception(sm_err);
+    stage("build_smoother", t0);  // what is left of it after the eigenproblems
     t0 = Clock::now();
     Level next;
     galerkin_gp(cur.G, cur.topo, cur.ip, next.G, s);

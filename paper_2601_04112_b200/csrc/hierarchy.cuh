@@ -56,6 +56,7 @@ struct Hierarchy {
   std::vector<StageTime> timings;
   int device = 0;
   cudaStream_t stream = nullptr;  // setup stream
+  cudaStream_t side_stream = nullptr;  // Schwarz-block factorisations (owns the smoothers' buffers)
   mutable std::mutex mu;          // guards lazily built export caches
   ~Hierarchy();
 };
