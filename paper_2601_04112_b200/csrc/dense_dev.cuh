@@ -724,43 +724,77 @@ __device__ void t_symmetrize(const Team& t, double* a, int n) {
   t.sync();
 }
 
+// Core of the dense products: c(i,j) = Σ_k a(i,k)·b(k,j) with k ascending, a(i,k) = a[i·sa_i + k·sa_k],
+// optionally skipping a(i,k) == 0 (select, not a branch, so the loads pipeline). A thread owns four
+// consecutive rows i of one column j: the b(k,j) load is shared and coalesced across the team, the
+// a loads are uniform across the lanes of a row block. Every sum keeps the reference's order.
+template <bool SKIP, class Team, class Store>
+__device__ __forceinline__ void t_mm_core(const Team& t, const double* a, int64_t sa_i, int64_t sa_k, int ar, int ac,
+                                          const double* b, int bc, Store store) {
+  const int rb = (ar + 3) >> 2;
+  const int64_t cnt = int64_t(rb) * bc;
+  for (int64_t e = t.rank(); e < cnt; e += t.size()) {
+    const int i0 = static_cast<int>(e / bc) << 2, j = static_cast<int>(e % bc);
+    const double* p0 = a + int64_t(i0) * sa_i;
+    const double* p1 = a + int64_t(min(i0 + 1, ar - 1)) * sa_i;
+    const double* p2 = a + int64_t(min(i0 + 2, ar - 1)) * sa_i;
+    const double* p3 = a + int64_t(min(i0 + 3, ar - 1)) * sa_i;
+    const double* pb = b + j;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < ac; ++k) {
+      const double bk = pb[int64_t(k) * bc];
+      const int64_t o = int64_t(k) * sa_k;
+      const double x0 = p0[o], x1 = p1[o], x2 = p2[o], x3 = p3[o];
+      if (SKIP) {
+        s0 = x0 != 0.0 ? s0 + x0 * bk : s0;
+        s1 = x1 != 0.0 ? s1 + x1 * bk : s1;
+        s2 = x2 != 0.0 ? s2 + x2 * bk : s2;
+        s3 = x3 != 0.0 ? s3 + x3 * bk : s3;
+      } else {
+        s0 += x0 * bk;
+        s1 += x1 * bk;
+        s2 += x2 * bk;
+        s3 += x3 * bk;
+      }
+    }
+    store(i0, j, s0);
+    if (i0 + 1 < ar) store(i0 + 1, j, s1);
+    if (i0 + 2 < ar) store(i0 + 2, j, s2);
+    if (i0 + 3 < ar) store(i0 + 3, j, s3);
+  }
+  t.sync();
+}
+
 // c(ar×bc) = a(ar×ac)·b(ac×bc), skipping a(i,k) == 0        dense.hpp:47-59
 template <class Team>
 __device__ void t_matmul(const Team& t, const double* a, int ar, int ac, const double* b, int bc, double* c) {
-  const int64_t cnt = int64_t(ar) * bc;
-  for (int64_t e = t.rank(); e < cnt; e += t.size()) {
-    const int i = static_cast<int>(e / bc), j = static_cast<int>(e % bc);
-    double s = 0.0;
-    for (int k = 0; k < ac; ++k) {
-      const double aik = a[int64_t(i) * ac + k];
-      if (aik == 0.0) continue;
-      s += aik * b[int64_t(k) * bc + j];
-    }
-    c[e] = s;
-  }
-  t.sync();
+  t_mm_core<true>(t, a, ac, 1, ar, ac, b, bc, [&](int i, int j, double v) { c[int64_t(i) * bc + j] = v; });
 }
 
 // c(ac×bc) = a(ar×ac)ᵀ·b(ar×bc), skipping a(k,i) == 0       dense.hpp:62-74
 template <class Team>
 __device__ void t_matmul_transa(const Team& t, const double* a, int ar, int ac, const double* b, int bc, double* c) {
-  const int64_t cnt = int64_t(ac) * bc;
-  for (int64_t e = t.rank(); e < cnt; e += t.size()) {
-    const int i = static_cast<int>(e / bc), j = static_cast<int>(e % bc);
-    double s = 0.0;
-    for (int k = 0; k < ar; ++k) {
-      const double aki = a[int64_t(k) * ac + i];
-      if (aki == 0.0) continue;
-      s += aki * b[int64_t(k) * bc + j];
-    }
-    c[e] = s;
-  }
-  t.sync();
+  t_mm_core<true>(t, a, 1, ac, ac, ar, b, bc, [&](int i, int j, double v) { c[int64_t(i) * bc + j] = v; });
 }
 
-// Sequential reductions by rank 0, broadcast through *slot.
+// Sequential reductions by rank 0, broadcast through *slot. With a shared-memory scratch `sm`
+// (n + 1 doubles) the team forms the products in parallel and rank 0 only runs the ordered sum.
 template <class Team>
-__device__ double t_seq_dot(const Team& t, const double* x, const double* y, int n, double* slot) {
+__device__ double t_seq_dot(const Team& t, const double* x, const double* y, int n, double* slot, double* sm = nullptr) {
+  if (sm) {
+    for (int i = t.rank(); i < n; i += t.size()) sm[i] = x[i] * y[i];
+    t.sync();
+    if (t.rank() == 0) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) s += sm[i];
+      sm[n] = s;
+    }
+    t.sync();
+    const double v = sm[n];
+    t.sync();
+    return v;
+  }
   if (t.rank() == 0) {
     double s = 0.0;
     for (int i = 0; i < n; ++i) s += x[i] * y[i];
@@ -785,7 +819,19 @@ __device__ int t_sym_eig(const Team& t, int n, const double* m, double* vals, do
   }
   if constexpr (!std::is_same<Team, WarpTeam>::value) {
     if (ar.wctl && n >= ar.wave_min && n <= kWaveMaxN && wave_smem_doubles(n) <= ar.fast_cap)
+    {
+#ifdef LSB_DIAG
+      const long long c0 = clock64();
+      const int st = wave_sym_eig_leader(n, m, vals, vecs, ar.wctl, ar.wws, ar.fast);
+      if (t.rank() == 0 && g_eig_prof) {  // diagnostics: cycles and calls of the wavefront eigensolves
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_eig_prof) + 4, static_cast<unsigned long long>(clock64() - c0));
+        atomicAdd(reinterpret_cast<unsigned long long*>(g_eig_prof) + 5, 1ull);
+      }
+      return st;
+#else
       return wave_sym_eig_leader(n, m, vals, vecs, ar.wctl, ar.wws, ar.fast);
+#endif
+    }
     if (std::is_same<Team, BlockTeam>::value && ar.fast && n >= 48 && blockDim.x == kPipeThreads) {
       int R = 8;
       while (R > 4 && pipelined_smem_doubles(n, R) > ar.fast_cap) R -= 2;
@@ -919,19 +965,20 @@ __device__ int t_pseudo_inverse(const Team& t, int n, const double* m, double ta
   if (st) return st;
   const double cut = n == 0 ? 0.0 : tau_rel * fmax(ev[n - 1], 0.0);
   const int64_t nn = int64_t(n) * n;
+  // out(i,j) = Σ_k (V(i,k)·(1/λ_k))·V(j,k) over λ_k > cut, skipping zero V(i,k)/λ_k. The reciprocals
+  // are taken once, V is scaled in place and read against a transposed copy (coalesced); a cut λ
+  // scales its column to ±0, which the product skips like the reference's `continue`.
+  double* vt = ar.take(nn);  // the eigensolver's scratch is free again
+  t.sync();
+  for (int k = t.rank(); k < n; k += t.size()) ev[k] = ev[k] <= cut ? 0.0 : 1.0 / ev[k];
   for (int64_t e = t.rank(); e < nn; e += t.size()) {
-    const int i = static_cast<int>(e / n), j = static_cast<int>(e % n);
-    double s = 0.0;
-    for (int k = 0; k < n; ++k) {
-      if (ev[k] <= cut) continue;
-      const double inv = 1.0 / ev[k];
-      const double vik = eV[int64_t(i) * n + k] * inv;
-      if (vik == 0.0) continue;
-      s += vik * eV[int64_t(j) * n + k];
-    }
-    out[e] = s;
+    const int k = static_cast<int>(e / n), j = static_cast<int>(e % n);
+    vt[e] = eV[int64_t(j) * n + k];
   }
   t.sync();
+  for (int64_t e = t.rank(); e < nn; e += t.size()) eV[e] *= ev[e % n];
+  t.sync();
+  t_matmul(t, eV, n, n, vt, n, out);
   return 0;
 }
 
@@ -955,7 +1002,19 @@ __device__ int t_spsd_gevp(const Team& t, int n, double* ls, double* bs, double 
   int n_null = 0;
   while (n_null < n && ebv[n_null] <= cut) ++n_null;
   const int n_ret = n - n_null;
-  if (t.rank() == 0) {  // frobenius_norm (dense.hpp:96-100)
+  if (ar.fast && ar.fast_cap >= 64) {  // frobenius_norm (dense.hpp:96-100): squares by the team, ordered sum by rank 0
+    const int64_t nn = int64_t(n) * n, cap = ar.fast_cap;
+    double s = 0.0;
+    for (int64_t e0 = 0; e0 < nn; e0 += cap) {
+      const int64_t len = nn - e0 < cap ? nn - e0 : cap;
+      for (int64_t e = t.rank(); e < len; e += t.size()) ar.fast[e] = ls[e0 + e] * ls[e0 + e];
+      t.sync();
+      if (t.rank() == 0)
+        for (int64_t e = 0; e < len; ++e) s += ar.fast[e];
+      t.sync();
+    }
+    if (t.rank() == 0) slot[0] = sqrt(s);
+  } else if (t.rank() == 0) {
     double s = 0.0;
     for (int64_t e = 0; e < int64_t(n) * n; ++e) s += ls[e] * ls[e];
     slot[0] = sqrt(s);
@@ -1012,16 +1071,12 @@ __device__ int t_spsd_gevp(const Team& t, int n, double* ls, double* bs, double 
     t_symmetrize(t, cm, n_ret);
     st = t_sym_eig(t, n_ret, cm, ecv, ecV, a2);
     if (st) return st;
-    for (int k = n_ret; k-- > 0;) {
-      double* u = outv + int64_t(cnt) * n;
-      for (int i = t.rank(); i < n; i += t.size()) {
-        double s = 0.0;
-        for (int j = 0; j < n_ret; ++j) s += w[int64_t(i) * n_ret + j] * ecV[int64_t(j) * n_ret + k];
-        u[i] = s;
-      }
-      if (t.rank() == 0) values[cnt] = ecv[k];
-      ++cnt;
-    }
+    // u_k = w·ecV(·,k), k descending: one product, vector k stored as output column cnt + (n_ret-1-k)
+    t_mm_core<false>(t, w, n_ret, 1, n, n_ret, ecV, n_ret, [&](int i, int k, double v) {
+      outv[int64_t(cnt + (n_ret - 1 - k)) * n + i] = v;
+    });
+    for (int k = t.rank(); k < n_ret; k += t.size()) values[cnt + (n_ret - 1 - k)] = ecv[k];
+    cnt += n_ret;
     t.sync();
   }
   *cnt_out = cnt;

@@ -278,17 +278,27 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
     }
     mark(1);
     // T = pinv·crossᵀ, S = cross·T (dense.hpp:47-59 with the transposed copy)
-    for (int64_t e = t.rank(); e < int64_t(ng) * nw; e += t.size()) {
-      const int i = static_cast<int>(e / nw), j = static_cast<int>(e % nw);
-      double s = 0.0;
-      for (int k = 0; k < ng; ++k) {
-        const double aik = Pm[int64_t(i) * ng + k];
-        if (aik == 0.0) continue;
-        s += aik * C[int64_t(j) * ng + k];
+    if (nw <= 2 * ng) {  // crossᵀ materialised in the eigensolver's scratch: coalesced reads
+      double* Ct = pa.take(int64_t(ng) * nw);
+      for (int64_t e = t.rank(); e < int64_t(ng) * nw; e += t.size()) {
+        const int k = static_cast<int>(e / nw), j = static_cast<int>(e % nw);
+        Ct[e] = C[int64_t(j) * ng + k];
       }
-      T[e] = s;
+      t.sync();
+      t_matmul(t, Pm, ng, ng, Ct, nw, T);
+    } else {
+      for (int64_t e = t.rank(); e < int64_t(ng) * nw; e += t.size()) {
+        const int i = static_cast<int>(e / nw), j = static_cast<int>(e % nw);
+        double s = 0.0;
+        for (int k = 0; k < ng; ++k) {
+          const double aik = Pm[int64_t(i) * ng + k];
+          if (aik == 0.0) continue;
+          s += aik * C[int64_t(j) * ng + k];
+        }
+        T[e] = s;
+      }
+      t.sync();
     }
-    t.sync();
     t_matmul(t, C, nw, ng, T, nw, S);
     for (int64_t e = t.rank(); e < int64_t(nw) * nw; e += t.size()) W[e] -= S[e];
     t.sync();
@@ -336,18 +346,19 @@ __device__ void gevp_problem(const Team& t, const GevpArgs& g, int idx, double* 
   if (keep == 0) keep = 1;
   if (keep > cnt) keep = cnt;
   int cols = 0;
+  double* const dsm = (fast && fast_cap >= nw + 1) ? fast : nullptr;  // shared scratch of the ordered dots
   for (int k = 0; k < keep; ++k) {
     for (int r = t.rank(); r < nw; r += t.size()) v[r] = outv[int64_t(k) * nw + r];
     t.sync();
-    const double orig = sqrt(t_seq_dot(t, v, v, nw, slot));
+    const double orig = sqrt(t_seq_dot(t, v, v, nw, slot, dsm));
     for (int pass = 0; pass < 2; ++pass)
       for (int c = 0; c < cols; ++c) {
         const double* pc = panel + int64_t(c) * nw;
-        const double proj = t_seq_dot(t, pc, v, nw, slot);
+        const double proj = t_seq_dot(t, pc, v, nw, slot, dsm);
         for (int r = t.rank(); r < nw; r += t.size()) v[r] -= proj * pc[r];
         t.sync();
       }
-    const double nv = sqrt(t_seq_dot(t, v, v, nw, slot));
+    const double nv = sqrt(t_seq_dot(t, v, v, nw, slot, dsm));
     if (!(nv > 1e-12 * fmax(orig, 1e-300))) continue;
     if (t.rank() == 0) {
       int arg = 0;
@@ -1478,7 +1489,8 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     long long* np = nullptr;
     LSB_CUDA(cudaMemcpyToSymbol(g_gevp_prof, &np, sizeof(np)));
     const auto he = eprof.download(s);
-    fprintf(stderr, "   large-n Jacobi steps %lld, rotations %lld\n", he[6], he[7]);
+    fprintf(stderr, "   large-n Jacobi steps %lld, rotations %lld; wavefront eigensolves %lld, %.1f Mcycles in total\n",
+            he[6], he[7], he[5], he[4] / 1e6);
     LSB_CUDA(cudaMemcpyToSymbol(g_eig_prof, &np, sizeof(np)));
   }
   if (LSB_DIAG_ENV("LSB_GRAM_CHECK") && pre.get()) {
