@@ -82,6 +82,9 @@ class DBuf {
   std::vector<T> download(cudaStream_t s) const {
     std::vector<T> h(n_);
     if (n_) {
+      // Wait for the stream first: a copy into pageable memory blocks inside the driver until the
+      // stream's earlier kernels finish, and other host threads' CUDA calls queue up behind it.
+      LSB_CUDA(cudaStreamSynchronize(s));
       LSB_CUDA(cudaMemcpyAsync(h.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost, s));
       LSB_CUDA(cudaStreamSynchronize(s));
     }
@@ -105,6 +108,7 @@ class DBuf {
 template <class T>
 T read_scalar(const T* d, cudaStream_t s) {
   T h{};
+  LSB_CUDA(cudaStreamSynchronize(s));  // see DBuf::download
   LSB_CUDA(cudaMemcpyAsync(&h, d, sizeof(T), cudaMemcpyDeviceToHost, s));
   LSB_CUDA(cudaStreamSynchronize(s));
   return h;

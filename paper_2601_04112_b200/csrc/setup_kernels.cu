@@ -448,8 +448,26 @@ __global__ void __launch_bounds__(512, 1) k_gevp_wave(GevpArgs g, WaveCtl* ctls,
   }
   ClusterLeadTeam t;
   double* ws = g.gws + int64_t(slot) * g.ws_stride;
-  for (int idx = slot; idx < g.n_list; idx += nslots)
+  // the list is sorted largest first; a cluster takes the next problem when it finishes one
+  __shared__ int s_idx;
+  (void)nslots;
+  for (;;) {
+    if (threadIdx.x == 0) s_idx = atomicAdd(&ctls[0].next, 1);
+    __syncthreads();
+    const int idx = s_idx;
+    __syncthreads();
+    if (idx >= g.n_list) break;
+#ifdef LSB_DIAG
+    if (threadIdx.x == 0 && ctl->n_done == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ctl->t_start));
+#endif
     gevp_problem(t, g, idx, ws, dyn_smem, kWaveSmemCap, ctl, wws + int64_t(slot) * wws_stride, wave_min);
+#ifdef LSB_DIAG
+    if (threadIdx.x == 0) {
+      ctl->n_done += 1;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ctl->t_end));
+    }
+#endif
+  }
   wave_quit(ctl);
 }
 
@@ -1246,6 +1264,14 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
                     const std::vector<int32_t>& hgo, const DevRowSets& rs, const std::vector<int64_t>& h_nz_off,
                     const GevpParams& gp, DevInterp& ip, DevCsr& p, bool keep_spectra, cudaStream_t s) {
   (void)h_nz_off;
+  const bool tprof = LSB_DIAG_ENV("LSB_STAGE_PROF");  // diagnostics: synchronised wall-clock marks
+  const auto tp0 = std::chrono::steady_clock::now();
+  auto tmark = [&](const char* what) {
+    if (!tprof) return;
+    cudaStreamSynchronize(s);
+    fprintf(stderr, "  local_gevp level %d: %-28s %8.1f ms\n", gp.level, what,
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tp0).count());
+  };
   const int64_t na = topo.n_agg;
   const int64_t maxrow = std::max<int64_t>(rs.max_row_nnz, 1);
   std::vector<int64_t> need(na), spec_off(na + 1, 0);
@@ -1301,6 +1327,7 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
       tiled_grams(gm, topo, hoo, hgo, rs, h_nzo, big, gp.variant == 1 ? 1 : 0, pre.get(), pre_off.get(), s);
     }
   }
+  tmark("tiled grams done");
   // chunk aggregates (id order) so the nω² panel scratch stays bounded
   const int64_t budget = int64_t(1) << 27;  // doubles (1 GiB)
   std::vector<int32_t> h_k(na, 0);
@@ -1326,6 +1353,18 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
       a0 = a1;
     }
   }
+  struct Fork {
+    cudaStream_t s = nullptr;
+    cudaEvent_t e = nullptr;
+    ~Fork() {
+      if (s) {
+        cudaStreamSynchronize(s);
+        cudaStreamDestroy(s);
+      }
+      if (e) cudaEventDestroy(e);
+    }
+  } fork;
+  constexpr int kSideSms = 4;  // SMs a cluster launch leaves to the side stream's small problems
   // first pass: run all chunks, keep each chunk's panels on the device
   std::vector<DBuf<double>> chunk_panels(chunks.size());
   std::vector<DBuf<int64_t>> chunk_off(chunks.size());
@@ -1391,7 +1430,18 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     g.pre = pre.get();
     g.pre_off = pre.get() ? pre_off.get() : nullptr;
     std::vector<int32_t> lo;
-    if (!aggs.empty()) launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, s);
+    // A few small subdomains beside a cluster class: they run on a side stream (launched first, on
+    // SMs the cluster launch leaves free) instead of holding the cluster kernels back.
+    const bool side = !big.empty() && (!aggs.empty() || !mid.empty());
+    cudaStream_t fs = s;
+    if (side) {
+      if (!fork.s) LSB_CUDA(cudaStreamCreateWithFlags(&fork.s, cudaStreamNonBlocking));
+      if (!fork.e) LSB_CUDA(cudaEventCreateWithFlags(&fork.e, cudaEventDisableTiming));
+      LSB_CUDA(cudaEventRecord(fork.e, s));  // the chunk's buffers and uploads are ordered on s
+      LSB_CUDA(cudaStreamWaitEvent(fork.s, fork.e, 0));
+      fs = fork.s;
+    }
+    if (!aggs.empty()) launch_classes(g, aggs, need, k_gevp_warp<4>, k_gevp_block<true>, k_gevp_block<false>, lo, fs);
     DBuf<int32_t> mid_list;
     DBuf<double> mid_ws;
     if (!mid.empty()) {
@@ -1404,15 +1454,15 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
       // 16 warps (problems) per SM; bound the footprint to ~2 GiB
       const int64_t slots = std::max<int64_t>(WPB, std::min<int64_t>({int64_t(ceil_div(cnt, WPB)) * WPB, int64_t(sm_count()) * 16,
                                                                       ((int64_t(1) << 28) / std::max<int64_t>(wmax, 1)) / WPB * WPB}));
-      mid_list.upload(mid, s);
-      mid_ws.alloc(slots * wmax, s);
+      mid_list.upload(mid, fs);
+      mid_ws.alloc(slots * wmax, fs);
       GevpArgs gm2 = g;
       gm2.list = mid_list.get();
       gm2.list_base = base;
       gm2.n_list = cnt;
       gm2.ws_stride = wmax;
       gm2.gws = mid_ws.get();
-      k_gevp_warp_g<WPB><<<static_cast<int>(slots / WPB), WPB * 32, 0, s>>>(gm2);
+      k_gevp_warp_g<WPB><<<static_cast<int>(slots / WPB), WPB * 32, 0, fs>>>(gm2);
       LSB_LAUNCH();
       lo.insert(lo.end(), mid.begin(), mid.end());
     }
@@ -1439,8 +1489,9 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
       wmax = r2(wmax);
       const int64_t wws = r2(wave_ws_doubles(nmax));
       // one cluster per slot; bound the footprint to ~2 GiB
-      const int64_t slots = std::max<int64_t>(1, std::min<int64_t>({int64_t(cnt), int64_t(sm_count()) / C,
+      int64_t slots = std::max<int64_t>(1, std::min<int64_t>({int64_t(cnt), int64_t(sm_count()) / C,
                                                                     (int64_t(1) << 28) / std::max<int64_t>(wmax + wws, 1)}));
+      if (side) slots = std::max<int64_t>(1, std::min<int64_t>(slots, (int64_t(sm_count()) - kSideSms) / C));
       big_lists.emplace_back();
       big_lists.back().upload(part, s);
       big_ws.emplace_back(slots * wmax, s);
@@ -1472,6 +1523,24 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
       LSB_CUDA(cudaLaunchKernelEx(&cfg, k_gevp_wave, gb, big_ctl.back().get(), wbuf, wws, static_cast<int>(kWaveMinN)));
       LSB_LAUNCH();
       lo.insert(lo.end(), part.begin(), part.end());
+      if (LSB_DIAG_ENV("LSB_WAVE_SLOTS")) {  // diagnostics: per-cluster activity window
+        const auto hc = big_ctl.back().download(s);
+        long long t0 = LLONG_MAX, t1 = 0;
+        for (const auto& c : hc)
+          if (c.n_done) {
+            t0 = std::min(t0, c.t_start);
+            t1 = std::max(t1, c.t_end);
+          }
+        fprintf(stderr, "wave class C=%d level %d: %lld problems, %lld slots, span %.1f ms; per slot (count start end ms):", C,
+                gp.level, (long long)cnt, (long long)slots, (t1 - t0) / 1e6);
+        for (const auto& c : hc)
+          fprintf(stderr, " %d:%.0f-%.0f", c.n_done, c.n_done ? (c.t_start - t0) / 1e6 : -1.0, c.n_done ? (c.t_end - t0) / 1e6 : -1.0);
+        fprintf(stderr, "\n");
+      }
+    }
+    if (side) {  // join before the chunk's buffers are released
+      LSB_CUDA(cudaEventRecord(fork.e, fork.s));
+      LSB_CUDA(cudaStreamWaitEvent(s, fork.e, 0));
     }
     chunk_list[ci].upload(lo, s);
   }
@@ -1503,6 +1572,7 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
     fprintf(stderr, "gram check level %d: %llu mismatches; first agg %llu mat %llu idx %llu team %.17g tiled %.17g\n",
             gp.level, hb[0], hb[1], hb[2], hb[3], va, vb);
   }
+  tmark("eigenproblem kernels done");
   const auto hs = status.download(s);
   for (int64_t i = 0; i < na; ++i) {
     if (hs[i] == 1) raise(LSAMGDD_ERR_EIG, "sym_eig: Jacobi iteration did not converge");
@@ -1560,6 +1630,7 @@ void local_gevp_all(const DevCsr& gm, const DevTopo& topo, const std::vector<int
                                             ip.panels.get(), ip.coarse_off.get(), p.off.get(), n, p.col.get(),
                                             p.val.get());
   LSB_LAUNCH();
+  tmark("panels and P assembled");
 }
 
 void coarse_factor(const DevCsr& a, DBuf<double>& inv, cudaStream_t s) {

@@ -21,3 +21,4 @@ for name, ms in h.timings():
     if name == "aggregation_topology":
         lvl += 1
     print(f"L{max(lvl, 0)} {name:24s} {ms:9.1f}")
+print("total_ms", round(sum(ms for _, ms in h.timings()), 1))
