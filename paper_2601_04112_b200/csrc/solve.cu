@@ -557,24 +557,34 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
       const int32_t* ids = reinterpret_cast<const int32_t*>(base + blk_cap) + lane;
       const int32_t* slots = reinterpret_cast<const int32_t*>(base + blk_cap + ids_cap) + lane;
       const int nr = MODE < 2 ? m : nw;
-      for (int j = cw; j < nr; j += kTmaConsumers) {
-        const int id = ids[j * 32];
-        rs[j * 32 + lane] = id >= 0 ? __ldcg(&r[id]) : 0.0;
-      }
-      cbar();
       const int p0 = nw * (nw + 1) / 2;
       const int nout = MODE < 2 ? nw : m;
       // this warp's rows: cw, cw + 9, …
       constexpr int kMaxRows = (kLaneMaxSub + kTmaConsumers - 1) / kTmaConsumers;
-      double eold[kMaxRows];
-      int outs[kMaxRows];
+      // Every global load of the group (the warp's share of the r gather and the old e of its ω rows)
+      // is issued before the first one is used: one trip to L2/HBM per group instead of one per row.
+      int gid[kMaxRows], outs[kMaxRows];
+      double gval[kMaxRows], eold[kMaxRows];
 #pragma unroll
       for (int q = 0; q < kMaxRows; ++q) {
         const int row = cw + q * kTmaConsumers;
+        gid[q] = row < nr ? ids[row * 32] : -1;
         // ω rows: the node; Γ rows of RAS-T: the slot of the contribution
         outs[q] = row < nout ? ((MODE == 2 && row >= nw) ? slots[(row - nw) * 32] : ids[row * 32]) : -1;
+      }
+#pragma unroll
+      for (int q = 0; q < kMaxRows; ++q) gval[q] = gid[q] >= 0 ? __ldcg(&r[gid[q]]) : 0.0;
+#pragma unroll
+      for (int q = 0; q < kMaxRows; ++q) {
+        const int row = cw + q * kTmaConsumers;
         eold[q] = (MODE != 0 && row < nw && outs[q] >= 0) ? e[outs[q]] : 0.0;
       }
+#pragma unroll
+      for (int q = 0; q < kMaxRows; ++q) {
+        const int row = cw + q * kTmaConsumers;
+        if (row < nr) rs[row * 32 + lane] = gval[q];
+      }
+      cbar();
 #pragma unroll
       for (int q = 0; q < kMaxRows; ++q) {
         const int row = cw + q * kTmaConsumers;
