@@ -435,6 +435,42 @@ def main() -> None:
     h2d = int(cfg.g_rowptr.nbytes + cfg.g_cols.nbytes + cfg.g_vals.nbytes + cfg.rhs.nbytes)
     d2h = int(8 * n)
 
+    # the same step with the factor written on the device (lsamgdd_generate_stencil_rows inside the
+    # timed region): only b goes up and x comes down
+    generated = None
+    stencil = configs.config_stencil(cfg.name, cfg.meta["grid"])
+    if stencil is not None:
+        def step_generated():
+            gd = lsamgdd.generate_stencil_rows(*stencil, device=local)
+            try:
+                h = C.c_void_p()
+                gcsr = gd.to_abi()
+                lsamgdd._check(lib.lsamgdd_setup(C.byref(gcsr), C.byref(pabi), C.byref(h), err, C.c_size_t(1024)), err)
+                rep = abi.Report()
+                st = lib.lsamgdd_pcg(h, None, C.c_void_p(h_b.data_ptr()), C.c_double(1e-8), C.c_uint64(1000),
+                                     C.c_void_p(h_x.data_ptr()), C.c_int32(abi.HOST), C.byref(rep), err, C.c_size_t(1024))
+                lib.lsamgdd_destroy(h)
+                lsamgdd._check(st, err)
+                return rep.iterations
+            finally:
+                gd.close()
+
+        gt = []
+        for _ in range(2):
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.cuda.synchronize()
+            its = step_generated()
+            e1.record()
+            torch.cuda.synchronize()
+            gt.append(e0.elapsed_time(e1))
+        gms = statistics.mean(gt)
+        generated = {"value": world * n / (gms / 1e3), "unit": UNIT, "ms_per_step": gms, "pcg_iterations": int(its),
+                     "h2d_bytes_per_step": int(cfg.rhs.nbytes), "d2h_bytes_per_step": int(8 * n),
+                     "note": "factor generated in HBM by lsamgdd_generate_stencil_rows inside the timed step "
+                             "(bit-identical to the host generator); host b in, host x out"}
+
     # dominant HBM kernel: level-0 Schwarz sweeps, CUDA events on their stream
     ks = abi.KernelStats()
     step(True, ks)
@@ -482,6 +518,8 @@ def main() -> None:
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if generated is not None:
+        out["e2e_device_generated"] = generated
     # the same stages on the GPU: level-0 setup stage timers + per-iteration event times of the
     # operator pair and the Schwarz pair (measured inside the captured PCG graph)
     st0 = infos[-1]["stages_list"]

@@ -261,6 +261,27 @@ int64_t lsamgdd_launch_count(void);
  * lsamgdd_cli.cpp:103-107; host only. */
 void lsamgdd_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out);
 
+/* On-device generator of a constant-coefficient grid factor (
+ * the constructions of BASELINE configs 2, 3 and 5 — SURVEY.md Appendix A.1 —
+ * and, with two rows per node, build_rotated_aniso of problems.hpp:106-132
+ * with its gradient rows of problems.hpp:84-104). The factor is written
+ * straight into device memory, so only the right-hand side crosses PCIe.
+ *   grid[3]      extents (nx, ny, nz), x fastest; node = (z*ny + y)*nx + x
+ *   offsets      [rows_per_node][max_entries][3] neighbour offsets (dx, dy, dz)
+ *   coefs        [rows_per_node][max_entries]; an exact 0.0 is no entry
+ * Row rows_per_node*node + k holds coefs[k][e] at column node + offset e for
+ * every neighbour inside the grid (homogeneous Dirichlet closure), columns
+ * ascending. rows_per_node, max_entries <= 8. *out_csr views device arrays
+ * (memory = LSAMGDD_DEVICE) owned by *out_owner; pass it to lsamgdd_setup /
+ * lsamgdd_pcg and release it with lsamgdd_generated_destroy afterwards. */
+int lsamgdd_generate_stencil_rows(const int64_t grid[3], int32_t rows_per_node, int32_t max_entries,
+                                  const int32_t* offsets, const double* coefs, int32_t device,
+                                  void** out_owner, lsamgdd_csr* out_csr, char* err, size_t errlen);
+/* Host copy of a generated factor (offsets n_rows+1, cols/values nnz; NULL skips an array). */
+int lsamgdd_generated_export(const void* owner, int64_t* offsets, int64_t* cols, double* values, char* err,
+                             size_t errlen);
+int lsamgdd_generated_destroy(void* owner);
+
 #ifdef __cplusplus
 }
 #endif

@@ -376,3 +376,84 @@ def config(name: str, scale: int | None = None, eps_perp: float = 1e-6) -> Confi
             meta=dict(grid=nn, eps=1e-4, alpha=math.pi / 4, beta=math.pi / 5, blocks="4x4x4", max_modes=12, seed=4),
         )
     raise ValueError(f"unknown config {name!r}")
+
+
+# ---- stencil-row descriptions for the on-device generator (lsamgdd_generate_stencil_rows) ----
+
+
+def rotated_aniso_2d_stencil(nx: int, ny: int, eps: float, theta: float):
+    """The factor of :func:`rotated_aniso_2d` as (grid, offsets[4][3][3], coefs[4][3]):
+    row 4·node + 2·half + d, same coefficient arithmetic, so the device-generated
+    CSR equals the host one bit for bit."""
+    h = 1.0 / (nx + 1)
+    hy = 1.0 / (ny + 1)
+    c, s = math.cos(theta), math.sin(theta)
+    se = math.sqrt(eps)
+    w = 1.0 / math.sqrt(2.0)
+    dirs = [(w * c, w * s), (w * se * -s, w * se * c)]
+    offsets = np.zeros((4, 3, 3), dtype=np.int32)
+    coefs = np.zeros((4, 3), dtype=np.float64)
+    for half in range(2):
+        for d, (bx, by) in enumerate(dirs):
+            k = 2 * half + d
+            cx, cy = bx / h, by / hy
+            if half == 0:
+                offsets[k] = [[0, 0, 0], [1, 0, 0], [0, 1, 0]]
+                coefs[k] = [-cx - cy, cx, cy]
+            else:
+                offsets[k] = [[0, 0, 0], [1, 0, 0], [0, -1, 0]]
+                coefs[k] = [-cx + cy, cx, -cy]
+    return (nx, ny, 1), offsets, coefs
+
+
+def rotated_aniso_3d_stencil(nn: int, eps: float, alpha: float, beta: float):
+    """The factor of :func:`rotated_aniso_3d` as (grid, offsets[3][4][3], coefs[3][4])."""
+    h = 1.0 / (nn + 1)
+    ca, sa, cb, sb = math.cos(alpha), math.sin(alpha), math.cos(beta), math.sin(beta)
+    rz = np.array([[ca, -sa, 0.0], [sa, ca, 0.0], [0.0, 0.0, 1.0]])
+    ry = np.array([[cb, 0.0, sb], [0.0, 1.0, 0.0], [-sb, 0.0, cb]])
+    R = rz @ ry
+    bt = np.diag([1.0, math.sqrt(eps), math.sqrt(eps)]) @ R.T
+    offsets = np.zeros((3, 4, 3), dtype=np.int32)
+    coefs = np.zeros((3, 4), dtype=np.float64)
+    for d in range(3):
+        coef = bt[d] / h
+        offsets[d] = [[0, 0, 0], [1, 0, 0], [0, 1, 0], [0, 0, 1]]
+        coefs[d] = [-coef.sum(), coef[0], coef[1], coef[2]]
+    return (nn, nn, nn), offsets, coefs
+
+
+def stencil_rows_host(grid, offsets: np.ndarray, coefs: np.ndarray):
+    """numpy statement of lsamgdd_generate_stencil_rows' contract (test helper):
+    neighbours outside the grid and exact zeros dropped, columns ascending."""
+    nx, ny, nz = (int(g) for g in grid)
+    n = nx * ny * nz
+    R, E = coefs.shape
+    node = np.arange(n, dtype=np.int64)
+    x, y, z = node % nx, (node // nx) % ny, node // (nx * ny)
+    rows_l, cols_l, vals_l = [], [], []
+    for k in range(R):
+        for e in range(E):
+            dx, dy, dz = (int(v) for v in offsets[k, e])
+            ok = (x + dx >= 0) & (x + dx < nx) & (y + dy >= 0) & (y + dy < ny) & (z + dz >= 0) & (z + dz < nz)
+            rows_l.append(R * node[ok] + k)
+            cols_l.append(node[ok] + (dz * ny + dy) * nx + dx)
+            vals_l.append(np.full(int(ok.sum()), coefs[k, e]))
+    rowptr, cc, vv = _assemble_rows(R * n, np.concatenate(rows_l), np.concatenate(cols_l), np.concatenate(vals_l), n)
+    return rowptr, cc, vv
+
+
+def config_stencil(name: str, scale: int | None = None):
+    """(grid, offsets, coefs) of a config whose factor the device can generate (c2, c3, c5), else None."""
+    name = name.lower()
+    if name == "c2":
+        nx = scale or 1024
+        return rotated_aniso_2d_stencil(nx, nx, 1e-3, math.pi / 6)
+    if name == "c3":
+        nx = scale or 4096
+        theta = float(mt19937_64_uniform(2, 1, 0.0, math.pi)[0])
+        return rotated_aniso_2d_stencil(nx, nx, 1e-6, theta)
+    if name == "c5":
+        nn = scale or 256
+        return rotated_aniso_3d_stencil(nn, 1e-4, math.pi / 4, math.pi / 5)
+    return None

@@ -9,6 +9,7 @@
 #include <new>
 #include <random>
 
+#include "generate.cuh"
 #include "hierarchy.cuh"
 
 using namespace lsb;
@@ -614,6 +615,31 @@ int lsamgdd_dense_sym_eig(int64_t n, const double* a, double* values, double* ve
 }
 
 int64_t lsamgdd_launch_count(void) { return launch_counter(); }
+
+int lsamgdd_generate_stencil_rows(const int64_t grid[3], int32_t rows_per_node, int32_t max_entries, const int32_t* offsets,
+                                  const double* coefs, int32_t device, void** out_owner, lsamgdd_csr* out_csr, char* err,
+                                  size_t errlen) {
+  if (out_owner) *out_owner = nullptr;
+  return guarded(err, errlen, [&] {
+    if (!out_owner || !out_csr) raise(LSAMGDD_ERR_INPUT, "generate_stencil_rows: null output argument");
+    require_device();
+    GeneratedCsr* g = generate_stencil_rows(grid, rows_per_node, max_entries, offsets, coefs, device);
+    generated_view(g, out_csr);
+    *out_owner = g;
+  });
+}
+
+int lsamgdd_generated_export(const void* owner, int64_t* offsets, int64_t* cols, double* values, char* err, size_t errlen) {
+  return guarded(err, errlen, [&] {
+    if (!owner) raise(LSAMGDD_ERR_INPUT, "null generated-matrix handle");
+    generated_export(static_cast<const GeneratedCsr*>(owner), offsets, cols, values);
+  });
+}
+
+int lsamgdd_generated_destroy(void* owner) {
+  generated_destroy(static_cast<GeneratedCsr*>(owner));
+  return LSAMGDD_OK;
+}
 
 void lsamgdd_uniform(uint64_t seed, double lo, double hi, int64_t n, double* out) {
   std::mt19937_64 gen(seed);

@@ -184,8 +184,62 @@ class SparseMatrix:
         return d
 
 
-def _as_sparse(g) -> SparseMatrix:
-    if isinstance(g, SparseMatrix):
+class DeviceSparseMatrix:
+    """Device-resident CSR written by the on-device generator
+    (lsamgdd_generate_stencil_rows); owns the device arrays. Accepted by
+    :func:`setup` and :func:`pcg` in place of a host :class:`SparseMatrix`."""
+
+    def __init__(self, owner: C.c_void_p, csr: abi.Csr):
+        self._owner = owner
+        self._csr = csr
+        self.n_rows, self.n_cols, self.nnz = int(csr.n_rows), int(csr.n_cols), int(csr.nnz)
+
+    def to_abi(self) -> abi.Csr:
+        if not self._owner:
+            raise InputError("generated matrix was closed")
+        return self._csr
+
+    def to_host(self) -> SparseMatrix:
+        off = np.empty(self.n_rows + 1, dtype=np.int64)
+        col = np.empty(self.nnz, dtype=np.int64)
+        val = np.empty(self.nnz, dtype=np.float64)
+        err = C.create_string_buffer(_ERRLEN)
+        _check(library().lsamgdd_generated_export(self._owner, abi.ptr(off), abi.ptr(col), abi.ptr(val), err,
+                                                  C.c_size_t(_ERRLEN)), err)
+        return SparseMatrix(self.n_rows, self.n_cols, off, col, val)
+
+    def close(self) -> None:
+        if self._owner:
+            library().lsamgdd_generated_destroy(self._owner)
+            self._owner = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def generate_stencil_rows(grid, offsets: np.ndarray, coefs: np.ndarray, device: int = 0) -> DeviceSparseMatrix:
+    """lsamgdd_generate_stencil_rows: the constant-coefficient grid factor of
+    BASELINE configs 2, 3, 5 written on the device (configs.config_stencil)."""
+    g = (C.c_int64 * 3)(*[int(v) for v in grid])
+    offsets = np.ascontiguousarray(offsets, dtype=np.int32)
+    coefs = np.ascontiguousarray(coefs, dtype=np.float64)
+    if offsets.ndim != 3 or offsets.shape[2] != 3 or coefs.shape != offsets.shape[:2]:
+        raise DimError("generate_stencil_rows: offsets must be [rows][entries][3] and coefs [rows][entries]")
+    owner = C.c_void_p()
+    csr = abi.Csr()
+    err = C.create_string_buffer(_ERRLEN)
+    lib = library()
+    _check(lib.lsamgdd_generate_stencil_rows(g, C.c_int32(coefs.shape[0]), C.c_int32(coefs.shape[1]), abi.ptr(offsets),
+                                             abi.ptr(coefs), C.c_int32(device), C.byref(owner), C.byref(csr), err,
+                                             C.c_size_t(_ERRLEN)), err)
+    return DeviceSparseMatrix(owner, csr)
+
+
+def _as_sparse(g):
+    if isinstance(g, (SparseMatrix, DeviceSparseMatrix)):
         return g
     if hasattr(g, "g_rowptr"):
         return SparseMatrix.from_arrays(g.g_rowptr, g.g_cols, g.g_vals, g.n)

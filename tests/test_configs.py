@@ -69,3 +69,16 @@ def test_partition_is_6x6_blocks_with_ragged_edge():
     sizes = np.bincount(part)
     assert sorted(set(sizes.tolist())) == [4, 12, 36]
     assert cfg.params == {"level0_overlap": 2}
+
+
+@pytest.mark.parametrize("name,scale", [("c2", 1), ("c2", 2), ("c2", 33), ("c3", 20), ("c5", 1), ("c5", 2), ("c5", 7)])
+def test_stencil_description_equals_host_generator(name, scale):
+    """configs.config_stencil (the input of the on-device generator,
+    lsamgdd_generate_stencil_rows) describes exactly the factor the host
+    generator assembles: same rows, columns and value bits."""
+    cfg = configs.config(name, scale)
+    grid, offsets, coefs = configs.config_stencil(name, scale)
+    rp, cc, vv = configs.stencil_rows_host(grid, offsets, coefs)
+    assert np.array_equal(rp, cfg.g_rowptr)
+    assert np.array_equal(cc, cfg.g_cols)
+    assert np.array_equal(vv, cfg.g_vals)

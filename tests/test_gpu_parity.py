@@ -506,3 +506,56 @@ def test_cli_report_schema_from_a_gpu_run(gpu, tmp_path):
     report.write_spectra_csv(h, str(path))
     lines = path.read_text().splitlines()
     assert lines[0] == "level,aggregate,index,eigenvalue" and len(lines) == 1 + 256 * 16
+
+
+@pytest.mark.parametrize("name,scale", [("c2", 1), ("c2", 2), ("c2", 64), ("c3", 96), ("c5", 2), ("c5", 12), ("c2", 1024)])
+def test_device_generated_factor_equals_host_generator(gpu, name, scale):
+    """lsamgdd_generate_stencil_rows: the factor written on the
+    device equals the host generator's CSR bit for bit — degenerate grids,
+    parity sizes and config 2 at its full 1024² size."""
+    cfg = configs.config(name, scale)
+    g = lsamgdd.generate_stencil_rows(*configs.config_stencil(name, scale))
+    try:
+        assert (g.n_rows, g.n_cols, g.nnz) == (cfg.m, cfg.n, cfg.nnz)
+        hst = g.to_host()
+        assert np.array_equal(hst.row_offsets, cfg.g_rowptr)
+        assert np.array_equal(hst.col_indices, cfg.g_cols)
+        assert np.array_equal(hst.values, cfg.g_vals)
+    finally:
+        g.close()
+
+
+def test_device_generator_rejects_bad_stencils(gpu):
+    off = np.zeros((1, 2, 3), dtype=np.int32)
+    with pytest.raises(lsamgdd.InputError):  # the same offset twice in a row
+        lsamgdd.generate_stencil_rows((4, 4, 1), off, np.ones((1, 2)))
+    with pytest.raises(lsamgdd.InputError):
+        lsamgdd.generate_stencil_rows((0, 4, 1), off[:, :1], np.ones((1, 1)))
+    with pytest.raises(lsamgdd.InputError):
+        lsamgdd.generate_stencil_rows((4, 4, 1), np.zeros((9, 1, 3), dtype=np.int32), np.ones((9, 1)))
+    with pytest.raises(lsamgdd.InputError):  # (-1, 1) and (1, 0) alias on a 2-wide grid
+        lsamgdd.generate_stencil_rows((2, 4, 1), np.array([[[-1, 1, 0], [1, 0, 0]]], dtype=np.int32), np.ones((1, 2)))
+
+
+def test_setup_and_solve_from_device_generated_factor(gpu):
+    """The whole path from a factor that never left the device: same hierarchy
+    bits, same PCG iterates as from the host CSR (config 2 at 96²)."""
+    cfg = configs.config("c2", 96)
+    p = lsamgdd.params_for(cfg)
+    h_host = lsamgdd.setup(cfg, p)
+    g = lsamgdd.generate_stencil_rows(*configs.config_stencil("c2", 96))
+    h_dev = lsamgdd.setup(g, p)
+    assert h_dev.num_levels == h_host.num_levels
+    for l in range(h_host.num_levels):
+        for what in ("A", "G"):
+            a, b = getattr(h_host.levels[l], what), getattr(h_dev.levels[l], what)
+            assert np.array_equal(a.row_offsets, b.row_offsets) and np.array_equal(a.col_indices, b.col_indices)
+            assert np.array_equal(a.values, b.values)
+    x0, r0 = lsamgdd.pcg(h_host, cfg.rhs, 1e-8, 200)
+    x1, r1 = lsamgdd.pcg(h_dev, cfg.rhs, 1e-8, 200)
+    assert r1.converged and r0.iterations == r1.iterations
+    assert np.array_equal(x0, x1)
+    x2, r2 = lsamgdd.pcg(h_host, cfg.rhs, 1e-8, 200, g0=g)
+    assert np.array_equal(x0, x2)
+    del h_dev
+    g.close()
