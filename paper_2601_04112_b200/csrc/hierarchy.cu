@@ -126,6 +126,13 @@ int64_t multi_pass_aggregation(const HostCsr& a, const DevCsr& dA, uint64_t pass
   return n_agg;
 }
 
+// host threads for the per-aggregate loops of the topology (independent aggregates)
+static int host_threads(int64_t n_items) {
+  const unsigned hc = std::thread::hardware_concurrency();
+  const int64_t cap = std::max<int64_t>(1, std::min<int64_t>(hc ? hc : 1, 16));
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(cap, n_items / 2048)));
+}
+
 // Γ sets, subdomain-intersection adjacency, greedy colouring
 // (aggregation.hpp:165-231; second Γ layer for the overlap-2 hook).
 void build_topology(const HostCsr& a, const std::vector<int64_t>& asg, int64_t n_agg, int layers, Level& L) {
@@ -154,27 +161,56 @@ void build_topology(const HostCsr& a, const std::vector<int64_t>& asg, int64_t n
   auto& gm = L.h_gamma;
   go.assign(n_agg + 1, 0);
   gm.clear();
-  std::vector<int32_t> buf, buf2;
-  for (int64_t i = 0; i < n_agg; ++i) {
-    buf.clear();
-    for (int32_t p = oo[i]; p < oo[i + 1]; ++p) {
-      const int64_t u = om[p];
-      for (int64_t k = a.off[u]; k < a.off[u + 1]; ++k)
-        if (asg[a.col[k]] != i) buf.push_back(static_cast<int32_t>(a.col[k]));
-    }
-    std::sort(buf.begin(), buf.end());
-    buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
-    if (layers >= 2) {
-      buf2 = buf;
-      for (int32_t u : buf)
+  // The Γ set of an aggregate depends on nothing but A and the partition: contiguous ranges of
+  // aggregates are built by host threads into their own buffers and concatenated in order.
+  auto gamma_range = [&](int64_t lo, int64_t hi, std::vector<int32_t>& out, std::vector<int32_t>& cnt) {
+    std::vector<int32_t> buf, buf2;
+    for (int64_t i = lo; i < hi; ++i) {
+      buf.clear();
+      for (int32_t p = oo[i]; p < oo[i + 1]; ++p) {
+        const int64_t u = om[p];
         for (int64_t k = a.off[u]; k < a.off[u + 1]; ++k)
-          if (asg[a.col[k]] != i) buf2.push_back(static_cast<int32_t>(a.col[k]));
-      std::sort(buf2.begin(), buf2.end());
-      buf2.erase(std::unique(buf2.begin(), buf2.end()), buf2.end());
-      buf.swap(buf2);
+          if (asg[a.col[k]] != i) buf.push_back(static_cast<int32_t>(a.col[k]));
+      }
+      std::sort(buf.begin(), buf.end());
+      buf.erase(std::unique(buf.begin(), buf.end()), buf.end());
+      if (layers >= 2) {
+        buf2 = buf;
+        for (int32_t u : buf)
+          for (int64_t k = a.off[u]; k < a.off[u + 1]; ++k)
+            if (asg[a.col[k]] != i) buf2.push_back(static_cast<int32_t>(a.col[k]));
+        std::sort(buf2.begin(), buf2.end());
+        buf2.erase(std::unique(buf2.begin(), buf2.end()), buf2.end());
+        buf.swap(buf2);
+      }
+      out.insert(out.end(), buf.begin(), buf.end());
+      cnt[i - lo] = static_cast<int32_t>(buf.size());
     }
-    gm.insert(gm.end(), buf.begin(), buf.end());
-    go[i + 1] = static_cast<int32_t>(gm.size());
+  };
+  const int nt = host_threads(n_agg);
+  {
+    std::vector<std::vector<int32_t>> parts(nt), cnts(nt);
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t) {
+      const int64_t lo = n_agg * t / nt, hi = n_agg * (t + 1) / nt;
+      cnts[t].assign(hi - lo, 0);
+      if (t + 1 < nt)
+        th.emplace_back(gamma_range, lo, hi, std::ref(parts[t]), std::ref(cnts[t]));
+      else
+        gamma_range(lo, hi, parts[t], cnts[t]);
+    }
+    for (auto& x : th) x.join();
+    size_t total = 0;
+    for (auto& x : parts) total += x.size();
+    gm.reserve(total);
+    int64_t i = 0;
+    for (int t = 0; t < nt; ++t) {
+      gm.insert(gm.end(), parts[t].begin(), parts[t].end());
+      for (int32_t c : cnts[t]) {
+        go[i + 1] = go[i] + c;
+        ++i;
+      }
+    }
   }
   // holders: owner first, then Γ-holders in ascending aggregate order
   std::vector<int64_t> hoff(n + 1, 0);
@@ -205,10 +241,18 @@ void build_topology(const HostCsr& a, const std::vector<int64_t>& asg, int64_t n
         }
   }
   std::vector<int64_t> deg(n_agg);
-  for (int64_t i = 0; i < n_agg; ++i) {
-    auto b = adj.begin() + aoff[i], e = adj.begin() + aoff[i + 1];
-    std::sort(b, e);
-    deg[i] = std::unique(b, e) - b;
+  {
+    auto sort_range = [&](int64_t lo, int64_t hi) {
+      for (int64_t i = lo; i < hi; ++i) {
+        auto b = adj.begin() + aoff[i], e = adj.begin() + aoff[i + 1];
+        std::sort(b, e);
+        deg[i] = std::unique(b, e) - b;
+      }
+    };
+    std::vector<std::thread> th;
+    for (int t = 0; t + 1 < nt; ++t) th.emplace_back(sort_range, n_agg * t / nt, n_agg * (t + 1) / nt);
+    sort_range(n_agg * (nt - 1) / nt, n_agg);
+    for (auto& x : th) x.join();
   }
   std::vector<int64_t> order(n_agg);
   std::iota(order.begin(), order.end(), 0);
