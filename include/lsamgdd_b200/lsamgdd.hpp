@@ -25,6 +25,7 @@
 // a move-only RAII handle; levels' host mirrors are fetched on request.
 #pragma once
 
+#include <array>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -220,7 +221,8 @@ class Hierarchy {
 inline std::size_t LevelsView::size() const { return h_->num_levels(); }
 inline const Level& LevelsView::operator[](std::size_t l) const { return h_->level_mirror(l); }
 
-inline Hierarchy setup(const SparseMatrix& g0, const LevelParams& params, const Extensions& ext = {}) {
+namespace detail {
+inline Hierarchy setup_csr(const lsamgdd_csr* g0, const LevelParams& params, const Extensions& ext) {
   lsamgdd_params p;
   lsamgdd_params_default(&p);
   p.max_levels = params.max_levels;
@@ -243,10 +245,9 @@ inline Hierarchy setup(const SparseMatrix& g0, const LevelParams& params, const 
   p.thresh_override = ext.thresh_override;
   p.level0_max_modes = ext.level0_max_modes;
   p.device = ext.device;
-  CsrView g(g0);
   void* h = nullptr;
   char err[1024];
-  check(lsamgdd_setup(&g.csr, &p, &h, err, sizeof err), err);
+  check(lsamgdd_setup(g0, &p, &h, err, sizeof err), err);
   Hierarchy out(h);
   out.params = params;
   if (!params.spectra_csv.empty()) {  // hierarchy.hpp:121-127, :163-165: level,aggregate,index,eigenvalue
@@ -263,6 +264,56 @@ inline Hierarchy setup(const SparseMatrix& g0, const LevelParams& params, const 
     }
   }
   return out;
+}
+}  // namespace detail
+
+inline Hierarchy setup(const SparseMatrix& g0, const LevelParams& params, const Extensions& ext = {}) {
+  CsrView g(g0);
+  return detail::setup_csr(&g.csr, params, ext);
+}
+
+// A factor written on the device by lsamgdd_generate_stencil_rows (the constant-coefficient grid
+// constructions of BASELINE configs 2, 3, 5; problems.hpp:84-132 has the same row shape): owns the
+// device arrays, converts to a host SparseMatrix on request.
+class DeviceFactor {
+ public:
+  // offsets: [rows_per_node][max_entries][3] (dx, dy, dz); coefs: [rows_per_node][max_entries], 0.0 = no entry
+  DeviceFactor(const std::array<int64_t, 3>& grid, int rows_per_node, int max_entries, const std::vector<int32_t>& offsets,
+               const std::vector<double>& coefs, int device = 0) {
+    if (offsets.size() != static_cast<std::size_t>(rows_per_node) * max_entries * 3 ||
+        coefs.size() != static_cast<std::size_t>(rows_per_node) * max_entries)
+      throw DimError("DeviceFactor: offsets must be [rows][entries][3] and coefs [rows][entries]");
+    char err[1024];
+    check(lsamgdd_generate_stencil_rows(grid.data(), rows_per_node, max_entries, offsets.data(), coefs.data(), device,
+                                        &owner_, &csr_, err, sizeof err),
+          err);
+  }
+  DeviceFactor(const DeviceFactor&) = delete;
+  DeviceFactor& operator=(const DeviceFactor&) = delete;
+  DeviceFactor(DeviceFactor&& o) noexcept : owner_(o.owner_), csr_(o.csr_) { o.owner_ = nullptr; }
+  ~DeviceFactor() {
+    if (owner_) lsamgdd_generated_destroy(owner_);
+  }
+  const lsamgdd_csr& csr() const { return csr_; }
+  std::size_t n_rows() const { return static_cast<std::size_t>(csr_.n_rows); }
+  std::size_t n_cols() const { return static_cast<std::size_t>(csr_.n_cols); }
+  std::size_t nnz() const { return static_cast<std::size_t>(csr_.nnz); }
+  SparseMatrix to_host() const {
+    std::vector<int64_t> off(n_rows() + 1), col(nnz());
+    std::vector<double> val(nnz());
+    char err[1024];
+    check(lsamgdd_generated_export(owner_, off.data(), col.data(), val.data(), err, sizeof err), err);
+    return SparseMatrix(n_rows(), n_cols(), std::vector<std::size_t>(off.begin(), off.end()),
+                        std::vector<std::size_t>(col.begin(), col.end()), std::move(val));
+  }
+
+ private:
+  void* owner_ = nullptr;
+  lsamgdd_csr csr_{};
+};
+
+inline Hierarchy setup(const DeviceFactor& g0, const LevelParams& params, const Extensions& ext = {}) {
+  return detail::setup_csr(&g0.csr(), params, ext);
 }
 
 inline Vector vcycle(const Hierarchy& h, std::size_t level, const Vector& r) {
@@ -294,6 +345,27 @@ inline std::pair<Vector, SolveReport> pcg(const Hierarchy& h, const SparseMatrix
   CsrView gv(g);
   char err[1024];
   check(lsamgdd_pcg(h.handle(), &gv.csr, b.data(), tol, maxit, x.data(), LSAMGDD_HOST, &rep, err, sizeof err), err);
+  SolveReport out;
+  out.iterations = rep.iterations;
+  out.converged = rep.converged != 0;
+  out.avg_conv_factor = rep.avg_conv_factor;
+  out.iters_to_tenth = rep.iters_to_tenth;
+  out.operator_complexity = rep.operator_complexity;
+  out.setup_seconds = rep.setup_seconds;
+  out.solve_seconds = rep.solve_seconds;
+  out.residual_history.assign(hist.begin(), hist.begin() + static_cast<std::ptrdiff_t>(rep.history_len));
+  return {std::move(x), std::move(out)};
+}
+
+// pcg with the factor the hierarchy was built from (no second copy of G: g == NULL in the C ABI)
+inline std::pair<Vector, SolveReport> pcg(const Hierarchy& h, const Vector& b, double tol = 1e-8, std::size_t maxit = 1000) {
+  Vector x(b.size());
+  std::vector<double> hist(maxit + 2);
+  lsamgdd_report rep{};
+  rep.residual_history = hist.data();
+  rep.history_capacity = hist.size();
+  char err[1024];
+  check(lsamgdd_pcg(h.handle(), nullptr, b.data(), tol, maxit, x.data(), LSAMGDD_HOST, &rep, err, sizeof err), err);
   SolveReport out;
   out.iterations = rep.iterations;
   out.converged = rep.converged != 0;

@@ -12,6 +12,7 @@ no CPU fallback — without the built library or a B200 every call raises.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 import os
 from dataclasses import dataclass, field
 from typing import Optional, Sequence
@@ -287,9 +288,18 @@ class Level:
     """Lazy host mirror of one device level (hierarchy.hpp:46-51)."""
 
     def __init__(self, h: "Hierarchy", index: int):
-        self._h = h
+        # weak: a strong reference would close a cycle (hierarchy -> levels -> hierarchy) and keep the
+        # device memory of a dropped hierarchy alive until the cycle collector happens to run
+        self._href = weakref.ref(h)
         self.index = index
         self._cache: dict = {}
+
+    @property
+    def _h(self) -> "Hierarchy":
+        h = self._href()
+        if h is None:
+            raise InputError("the hierarchy of this level was released")
+        return h
 
     def _csr(self, what: int) -> SparseMatrix:
         if what not in self._cache:
