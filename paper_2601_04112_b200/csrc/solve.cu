@@ -280,6 +280,15 @@ __device__ __forceinline__ double lrow_fixed(const int32_t* __restrict__ ids, co
 // Launch with programmatic stream serialization (PDL): the kernel's
 // griddepcontrol.wait orders it after its predecessor, while its launch and
 // CTA rasterisation overlap the predecessor's drain.
+static bool pdl_enabled() {
+#ifdef LSB_DIAG  // make DIAG=1: LSB_NO_PDL=1 launches the sweeps without programmatic dependent launch
+  static const bool on = getenv("LSB_NO_PDL") == nullptr;
+  return on;
+#else
+  return true;
+#endif
+}
+
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Args... args) {
   cudaLaunchConfig_t cfg = {};
@@ -290,7 +299,7 @@ void launch_pdl(void (*kern)(KArgs...), int grid, int block, cudaStream_t s, Arg
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   LSB_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
 }
 
@@ -516,6 +525,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     for (int k = 0; k < n_stage; ++k) {
       s_mbar_init(&full[k], 1);
       s_mbar_init(&empty[k], kTmaConsumers);
+      meta[k] = make_int4(0, 0, -1, 0);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -531,7 +541,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const uint32_t ib = static_cast<uint32_t>((v.g_ids_off[g + 1] - i0) * 4);
         const int64_t s0 = MODE == 2 ? v.g_slot_off[g] : 0;
         const uint32_t sb = MODE == 2 ? static_cast<uint32_t>((v.g_slot_off[g + 1] - s0) * 4) : 0u;
-        const int4 mt = make_int4(v.g_nw[g], v.g_ng[g], 0, 0);
+        const int4 mt = make_int4(v.g_nw[g], v.g_ng[g], k, 0);  // .z: the sequence number the consumers check
         if (k >= n_stage) s_mbar_wait(&empty[st], ((k / n_stage) - 1) & 1);
         meta[st] = mt;
         unsigned char* dst = stages + int64_t(st) * stage_bytes;
@@ -549,6 +559,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     int k = team;
     for (int64_t g = blockIdx.x + int64_t(team) * gridDim.x; g < ng_total; g += int64_t(kTmaTeams) * gridDim.x, k += kTmaTeams) {
       const int st = k % n_stage;
+      // A stage's phases are consumed by the three teams in turn, so a team does not observe every
+      // phase of its `full` barrier, and a parity wait alone cannot tell "phase k/n_stage complete"
+      // from "two phases behind" (a fill that completes late while this team has already finished
+      // its previous group: the parities coincide and the team would read a stage still being
+      // filled for an earlier group). The producer tags the stage with the group's sequence number
+      // before it arms the barrier; the parity wait starts only once the tag is this team's group.
+      {
+        const volatile int* seq = reinterpret_cast<const volatile int*>(&meta[st]) + 2;
+        while (*seq != k) __nanosleep(20);
+      }
       s_mbar_wait(&full[st], (k / n_stage) & 1);
       const int4 mt = meta[st];
       const int nw = mt.x, ngm = mt.y, m = nw + ngm;
@@ -660,6 +680,10 @@ __global__ void __launch_bounds__(256) k_rast_slots(const int32_t* __restrict__ 
 template <int MODE>
 bool schwarz_tma_launch(const SchwarzView& v, const double* r, double* e, cudaStream_t s) {
   if (v.n_groups == 0 || v.stage_blk_bytes == 0) return false;
+#ifdef LSB_DIAG  // make DIAG=1: LSB_NO_TMA=1 falls back to the lane-layout sweeps (k_schwarz_lrow)
+  static const bool no_tma = getenv("LSB_NO_TMA") != nullptr;
+  if (no_tma) return false;
+#endif
   if (MODE == 2 && (!v.rast_tmp || v.n_slots == 0)) return false;
   const int blk_cap = static_cast<int>((v.stage_blk_bytes + 127) & ~int64_t(127));
   const int ids_cap = static_cast<int>((v.stage_ids_bytes + 127) & ~int64_t(127));
@@ -684,7 +708,7 @@ bool schwarz_tma_launch(const SchwarzView& v, const double* r, double* e, cudaSt
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   LSB_CUDA(cudaLaunchKernelEx(&cfg, k_schwarz_tma<MODE>, v, r, e, v.rast_tmp, n_stage, stage_bytes, blk_cap, ids_cap, rs_rows));
   LSB_LAUNCH();
   if (MODE == 2) {
