@@ -417,11 +417,12 @@ void schwarz_lrow_launch(const SchwarzView& v, const int32_t* items, int64_t i0,
 // compute one output row per warp and lane (lane = aggregate of the group)
 // from the staged block and release the stage. HBM sees only long bulk reads;
 // the LSU handles just the r gather and the e scatter.
-// RAS-T (MODE 2) adds into e over the overlapping Ω sets: a group adds only
-// after every group of the earlier colours has added (per-colour completion
-// counters in global memory, reset by the last CTA), which keeps the
-// colour-ordered, deterministic sums of the multi-launch version in one launch
-// while the bulk copies of the next colour's groups keep streaming.
+// RAS-T (MODE 2): the ω rows add into e directly (interiors are disjoint), the Γ
+// rows store their contributions into per-node slots that k_rast_slots sums in
+// ascending holder order afterwards — one launch, no ordering between groups,
+// deterministic sums. The stage ring is shared by the consumer teams; the
+// producer tags each stage with its group's sequence number so that a team's
+// mbarrier parity wait cannot alias a phase another team has yet to consume.
 constexpr int kTmaConsumers = 9;  // consumer warps per team
 constexpr int kTmaTeams = 3;      // consumer teams; team t takes this CTA's groups k ≡ t (mod 3)
 constexpr int kTmaThreads = (kTmaTeams * kTmaConsumers + 1) * 32;  // + one producer warp
