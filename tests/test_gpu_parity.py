@@ -559,3 +559,22 @@ def test_setup_and_solve_from_device_generated_factor(gpu):
     assert np.array_equal(x0, x2)
     del h_dev
     g.close()
+
+
+@pytest.mark.parametrize("name,scale,over,reps", [("c1", 64, {}, 20), ("c2", 384, {}, 12), ("c3", 128, {"thresh_override": 10.0}, 20),
+                                                   ("c4", 48, {}, 20), ("c5", 12, {}, 20)])
+def test_reruns_are_bit_identical(gpu, name, scale, over, reps):
+    """Determinism of the solve on every sweep layout (TMA stage ring with its sequence tags at
+    C2 384², row layouts and colour-ordered RAS-T elsewhere): repeated V-cycles and PCG solves on
+    one hierarchy return the same bits (scripts/det_setup_stress.py is the long version that
+    exposed the stage-ring race, profiles/round2.md §16)."""
+    cfg = configs.config(name, scale)
+    h = lsamgdd.setup(cfg, lsamgdd.params_for(cfg, **over))
+    v0 = lsamgdd.vcycle(h, cfg.rhs)
+    x0, rep0 = lsamgdd.pcg(h, cfg.rhs, 1e-8, 1000)
+    assert rep0.converged
+    for _ in range(reps):
+        assert np.array_equal(lsamgdd.vcycle(h, cfg.rhs), v0)
+        x, rep = lsamgdd.pcg(h, cfg.rhs, 1e-8, 1000)
+        assert rep.iterations == rep0.iterations and np.array_equal(x, x0)
+        assert np.array_equal(rep.residual_history, rep0.residual_history)
