@@ -256,6 +256,14 @@ int lsamgdd_dense_sym_eig(int64_t n, const double* a, double* values, double* ve
  * replays counted per captured kernel). The bench's gpu_launches claim. */
 int64_t lsamgdd_launch_count(void);
 
+/* Device memory: every buffer of the library comes from a memory pool it owns
+ * (one per device, stream-ordered). Freed blocks stay mapped between calls, so
+ * a second setup does not pay for mapping its workspaces again; the host
+ * application's default pool and its release threshold are not touched. This
+ * call synchronises the device and returns the cached, unused memory to the
+ * driver (live hierarchies keep theirs). */
+int lsamgdd_trim_memory(int32_t device);
+
 /* ---- synthetic inputs (BASELINE.json configs) ---- */
 /* mt19937_64(seed) + uniform_real_distribution(lo,hi), the CLI recipe of
  * lsamgdd_cli.cpp:103-107; host only. */

@@ -616,6 +616,13 @@ int lsamgdd_dense_sym_eig(int64_t n, const double* a, double* values, double* ve
 
 int64_t lsamgdd_launch_count(void) { return launch_counter(); }
 
+int lsamgdd_trim_memory(int32_t device) {
+  return guarded(nullptr, 0, [&] {
+    LSB_CUDA(cudaSetDevice(device));
+    trim_device_pool(device);
+  });
+}
+
 int lsamgdd_generate_stencil_rows(const int64_t grid[3], int32_t rows_per_node, int32_t max_entries, const int32_t* offsets,
                                   const double* coefs, int32_t device, void** out_owner, lsamgdd_csr* out_csr, char* err,
                                   size_t errlen) {

@@ -43,7 +43,14 @@ inline int64_t& launch_counter() {
     ::lsb::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
   } while (0)
 
-// Stream-ordered device buffer (cudaMallocAsync on the owner's stream).
+// The library's own memory pool of the current device: every DBuf comes from it. Freed blocks stay
+// mapped between calls (release threshold = max, like a caching allocator), so repeated setups do
+// not pay for remapping tens of GB each time and the host application's default pool and its
+// release threshold are left alone; lsamgdd_trim_memory hands the cached memory back.
+cudaMemPool_t device_pool();
+void trim_device_pool(int device);
+
+// Stream-ordered device buffer (cudaMallocFromPoolAsync on the owner's stream).
 template <class T>
 class DBuf {
  public:
@@ -64,7 +71,7 @@ class DBuf {
     release();
     stream_ = s;
     n_ = n;
-    if (n) LSB_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), s));
+    if (n) LSB_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), device_pool(), s));
   }
   void release() {
     if (p_) cudaFreeAsync(p_, stream_);

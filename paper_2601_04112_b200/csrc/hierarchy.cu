@@ -422,26 +422,6 @@ Hierarchy* setup(const lsamgdd_csr* g0, const lsamgdd_params* p) {
   h->ratios.assign(p->coarsening_ratios, p->coarsening_ratios + p->n_ratios);
   h->device = p->device;
   LSB_CUDA(cudaSetDevice(p->device));
-  // Keep freed stream-ordered memory mapped while this setup runs: it allocates
-  // and frees hundreds of MB of per-level workspace, and returning it to the
-  // driver at every synchronisation costs seconds of remapping. The host
-  // application's own threshold is put back when setup returns.
-  struct PoolKeep {
-    cudaMemPool_t pool = nullptr;
-    uint64_t old = 0;
-    explicit PoolKeep(int device) {
-      if (cudaDeviceGetDefaultMemPool(&pool, device) != cudaSuccess) {
-        pool = nullptr;
-        return;
-      }
-      cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old);
-      uint64_t keep = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-    }
-    ~PoolKeep() {
-      if (pool) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &old);
-    }
-  } pool_keep(p->device);
   LSB_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   cudaStream_t s = h->stream;
   LSB_CUDA(cudaStreamCreateWithFlags(&h->side_stream, cudaStreamNonBlocking));

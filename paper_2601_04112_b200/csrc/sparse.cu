@@ -5,6 +5,8 @@
 // products and sums round exactly as in the reference's no-FMA Release build.
 #include <cub/cub.cuh>
 
+#include <mutex>
+
 #include <algorithm>
 
 #include "sparse.cuh"
@@ -255,6 +257,39 @@ int sm_count() {
     cache[dev].store(v, std::memory_order_relaxed);
   }
   return v;
+}
+
+namespace {
+std::mutex g_pool_mu;
+cudaMemPool_t g_pools[64] = {};
+}  // namespace
+
+cudaMemPool_t device_pool() {
+  int dev = 0;
+  LSB_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) raise(LSAMGDD_ERR_CUDA, "device ordinal out of range");
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (!g_pools[dev]) {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.handleTypes = cudaMemHandleTypeNone;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t pool = nullptr;
+    LSB_CUDA(cudaMemPoolCreate(&pool, &props));
+    uint64_t keep = UINT64_MAX;
+    LSB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+    g_pools[dev] = pool;
+  }
+  return g_pools[dev];
+}
+
+void trim_device_pool(int device) {
+  std::lock_guard<std::mutex> lk(g_pool_mu);
+  if (device >= 0 && device < 64 && g_pools[device]) {
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(g_pools[device], 0);
+  }
 }
 
 bool first_on_device(std::atomic<uint64_t>& flags) {
