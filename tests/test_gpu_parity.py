@@ -578,3 +578,20 @@ def test_reruns_are_bit_identical(gpu, name, scale, over, reps):
         x, rep = lsamgdd.pcg(h, cfg.rhs, 1e-8, 1000)
         assert rep.iterations == rep0.iterations and np.array_equal(x, x0)
         assert np.array_equal(rep.residual_history, rep0.residual_history)
+
+
+def test_trim_memory_returns_cached_blocks(gpu):
+    """lsamgdd_trim_memory: the library-owned pool gives its cached blocks back and keeps working."""
+    import ctypes as C
+    cfg = configs.config("c2", 192)
+    p = lsamgdd.params_for(cfg)
+    h = lsamgdd.setup(cfg, p)
+    x0, _ = lsamgdd.pcg(h, cfg.rhs, 1e-8, 500)
+    del h
+    assert lsamgdd.library().lsamgdd_trim_memory(C.c_int32(0)) == 0
+    h = lsamgdd.setup(cfg, p)
+    x1, _ = lsamgdd.pcg(h, cfg.rhs, 1e-8, 500)
+    assert np.array_equal(x0, x1)
+    assert lsamgdd.library().lsamgdd_trim_memory(C.c_int32(0)) == 0  # a live hierarchy keeps its memory
+    x2, _ = lsamgdd.pcg(h, cfg.rhs, 1e-8, 500)
+    assert np.array_equal(x0, x2)
